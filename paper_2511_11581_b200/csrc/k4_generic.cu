@@ -1,0 +1,177 @@
+// K4 -- generic SIMT Q-block kernel (§4.4 Q-Block; App. B).
+//
+// The exact-ish path: fp32 inputs (tolerance 1e-5, no tf32) and the fallback for bf16
+// shapes the specialised kernels do not cover (block sizes that are not a multiple of
+// 16, head_dim 64 prefill).  One CTA (4 warps) processes one work item = (Q block,
+// KV head): BLOCK_M = BLOCK_Q * G rows, token-major / head-minor (row r -> token
+// r / G, head kvh*G + r % G; reading R8).  K/V tiles of 32 keys are gathered through
+// the block table into shared memory ONCE per Q block and reused by all
+// rows (the Q-block arithmetic-density argument); every row runs the
+// online softmax of P:249-266 (m, l, acc in registers, division delayed to the end)
+// with its own causal limit ctx + i + 1.
+//
+// Persistent grid (static launch grid): CTAs stride over the
+// total_q_blocks * Hkv items produced by K5, last Q blocks first (longest first).
+#include <cfloat>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace pattn {
+namespace {
+
+constexpr int kWarps = 4;
+constexpr int kTileKeys = 32;
+
+template <typename T, int D, int RPW>
+__global__ void __launch_bounds__(kWarps * 32) k4_generic(Params p) {
+  extern __shared__ float smem[];
+  constexpr int DV = D / 32;  // accumulator elements per lane
+  const int G = p.G, BQ = p.block_q, BM = BQ * G;
+  float* sQ = smem;                        // [BM][D]
+  float* sK = sQ + BM * D;                 // [32][D+1]  (padded: lane-per-key reads conflict-free)
+  float* sV = sK + kTileKeys * (D + 1);    // [32][D]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const T* __restrict__ Q = static_cast<const T*>(p.q);
+  const T* __restrict__ K = static_cast<const T*>(p.k);
+  const T* __restrict__ V = static_cast<const T*>(p.v);
+  T* __restrict__ O = static_cast<T*>(p.out);
+
+  const int total_qb = p.hdr[kHdrTotalQBlocks];
+  const int n_items = total_qb * p.Hkv;
+  for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+    const int j = total_qb - 1 - it / p.Hkv;  // global Q-block id, last first
+    const int kvh = it % p.Hkv;
+    const int b = upper_bound_minus1(p.cu_qb, p.B, j);  // App. B P:46 binary search
+    const int qblk = j - p.cu_qb[b];
+    const int q0 = p.cu_seqlens_q[b];
+    const int qlen = p.cu_seqlens_q[b + 1] - q0;
+    const int L = p.seq_lens[b];
+    const int ctx = L - qlen;
+    const int tok0 = qblk * BQ;
+    const int ntok = min(BQ, qlen - tok0);
+    const int kv_end = ctx + tok0 + ntok;  // keys visible to the last row of the block
+    const int32_t* bt = p.block_table + (int64_t)b * p.bt_stride;
+
+    __syncthreads();  // previous item finished with sQ
+    for (int idx = threadIdx.x; idx < BM * D; idx += kWarps * 32) {
+      int r = idx / D, d = idx - r * D;
+      int tk = r / G;
+      float x = 0.f;
+      if (tk < ntok) {
+        int h = kvh * G + (r - tk * G);
+        x = to_f32(Q[(int64_t)(q0 + tok0 + tk) * p.q_st_tok + (int64_t)h * p.q_st_head + d]);
+      }
+      sQ[idx] = x;
+    }
+
+    float m[RPW], l[RPW], acc[RPW][DV];
+#pragma unroll
+    for (int i = 0; i < RPW; ++i) {
+      m[i] = -INFINITY;
+      l[i] = 0.f;
+#pragma unroll
+      for (int k = 0; k < DV; ++k) acc[i][k] = 0.f;
+    }
+
+    for (int t0 = 0; t0 < kv_end; t0 += kTileKeys) {
+      __syncthreads();
+      for (int idx = threadIdx.x; idx < kTileKeys * D; idx += kWarps * 32) {
+        int jj = idx / D, d = idx - jj * D;
+        int t = t0 + jj;
+        float kx = 0.f, vx = 0.f;
+        if (t < kv_end) {  // never touch slots past the visible range (may hold NaN, reading R13)
+          int64_t off = (int64_t)bt[t / p.bs] * p.kv_st_blk + (int64_t)(t % p.bs) * p.kv_st_tok +
+                        (int64_t)kvh * p.kv_st_head + d;
+          kx = to_f32(K[off]);
+          vx = to_f32(V[off]);
+        }
+        sK[jj * (D + 1) + d] = kx;
+        sV[jj * D + d] = vx;
+      }
+      __syncthreads();
+
+#pragma unroll
+      for (int i = 0; i < RPW; ++i) {
+        const int r = warp + i * kWarps;
+        if (r >= BM) break;
+        const int tk = r / G;
+        if (tk >= ntok) continue;
+        const int row_end = ctx + tok0 + tk + 1;  // keys 0 .. ctx+i (self-inclusive)
+        if (t0 >= row_end) continue;              // warp-uniform
+        const int t = t0 + lane;
+        float s = -INFINITY;
+        if (t < row_end) {
+          const float* qr = sQ + r * D;
+          const float* kr = sK + lane * (D + 1);
+          float dot = 0.f;
+#pragma unroll 16
+          for (int d = 0; d < D; ++d) dot = fmaf(qr[d], kr[d], dot);
+          s = dot * p.scale_log2;  // log2 domain: e^{x} = 2^{x log2 e}
+        }
+        const float m_new = fmaxf(m[i], warp_max(s));
+        const float alpha = exp2f(m[i] - m_new);  // m = -inf -> 0
+        const float pe = (t < row_end) ? exp2f(s - m_new) : 0.f;
+        l[i] = l[i] * alpha + warp_sum(pe);
+#pragma unroll
+        for (int k = 0; k < DV; ++k) acc[i][k] *= alpha;
+#pragma unroll 8
+        for (int jj = 0; jj < kTileKeys; ++jj) {
+          const float pj = __shfl_sync(0xffffffffu, pe, jj);
+          const float* vr = sV + jj * D + lane;
+#pragma unroll
+          for (int k = 0; k < DV; ++k) acc[i][k] = fmaf(pj, vr[32 * k], acc[i][k]);
+        }
+        m[i] = m_new;
+      }
+    }
+
+#pragma unroll
+    for (int i = 0; i < RPW; ++i) {
+      const int r = warp + i * kWarps;
+      if (r >= BM) break;
+      const int tk = r / G;
+      if (tk >= ntok) continue;
+      const int h = kvh * G + (r - tk * G);
+      T* o = O + (int64_t)(q0 + tok0 + tk) * p.o_st_tok + (int64_t)h * p.o_st_head;
+      const float inv = 1.f / l[i];
+#pragma unroll
+      for (int k = 0; k < DV; ++k) o[lane + 32 * k] = from_f32<T>(acc[i][k] * inv);
+    }
+  }
+}
+
+template <typename T, int D, int RPW>
+cudaError_t launch_t(const Params& p, int grid, cudaStream_t stream) {
+  size_t smem = generic_smem_bytes(p);
+  auto kern = k4_generic<T, D, RPW>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  kern<<<grid, kWarps * 32, smem, stream>>>(p);
+  return cudaGetLastError();
+}
+
+template <typename T, int D>
+cudaError_t launch_d(const Params& p, int grid, int rpw, cudaStream_t stream) {
+  return rpw <= 8 ? launch_t<T, D, 8>(p, grid, stream) : launch_t<T, D, 16>(p, grid, stream);
+}
+
+}  // namespace
+
+size_t generic_smem_bytes(const Params& p) {
+  const int BM = p.block_q * p.G;
+  return sizeof(float) * ((size_t)BM * p.D + (size_t)kTileKeys * (p.D + 1) + (size_t)kTileKeys * p.D);
+}
+
+cudaError_t launch_generic(const Params& p, int grid, int rows_per_warp, cudaStream_t stream) {
+  if (p.dtype == 0) {
+    if (p.D == 64) return launch_d<float, 64>(p, grid, rows_per_warp, stream);
+    if (p.D == 128) return launch_d<float, 128>(p, grid, rows_per_warp, stream);
+  } else {
+    if (p.D == 64) return launch_d<__nv_bfloat16, 64>(p, grid, rows_per_warp, stream);
+    if (p.D == 128) return launch_d<__nv_bfloat16, 128>(p, grid, rows_per_warp, stream);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace pattn

@@ -1,0 +1,42 @@
+// kernels.h -- host-callable launchers of the libpattn kernels (internal; not part of the C ABI).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "params.h"
+
+namespace pattn {
+
+// K5: batch metadata + decode segment plan (one CTA).
+cudaError_t launch_metadata(const Params& p, cudaStream_t stream);
+
+// K4: generic SIMT Q-block kernel (fp32 / bf16, any q_len, any block size).
+// rows_per_warp in {8, 16}: BLOCK_M = block_q * G <= 4 * rows_per_warp.
+cudaError_t launch_generic(const Params& p, int grid, int rows_per_warp, cudaStream_t stream);
+size_t generic_smem_bytes(const Params& p);
+
+// K2: split-KV decode kernel (bf16, TMA-fed shared-memory ring, mma.sync dot products).
+struct DecodeLaunch {
+  int grid;
+  int stages;
+  int consumer_warps;
+  size_t smem;
+};
+DecodeLaunch plan_decode(const Params& p, int num_sms, size_t max_smem);
+cudaError_t launch_decode(const Params& p, const DecodeLaunch& dl, const CUtensorMap& tmK, const CUtensorMap& tmV,
+                          cudaStream_t stream);
+
+// K3: segment reduction (LSE merge of decode partials).
+cudaError_t launch_reduce(const Params& p, cudaStream_t stream);
+
+// K1: tcgen05/TMEM prefill Q-block kernel (bf16, D = 128).
+struct PrefillLaunch {
+  int grid;
+  size_t smem;
+};
+bool prefill_supported(const Params& p);
+PrefillLaunch plan_prefill(const Params& p, int num_sms);
+cudaError_t launch_prefill(const Params& p, const PrefillLaunch& pl, const CUtensorMap& tmQ, const CUtensorMap& tmK,
+                           const CUtensorMap& tmV, cudaStream_t stream);
+
+}  // namespace pattn

@@ -1,0 +1,58 @@
+// params.h -- kernel parameter block and workspace layout shared by the host planner
+// (pattn_api.cu) and the kernels.  Plain C++ (no CUDA types) so the host side can
+// include it anywhere.
+#pragma once
+#include <stdint.h>
+
+namespace pattn {
+
+// Workspace header (int32 words), written by the metadata kernel K5.
+enum HdrWord {
+  kHdrTotalQBlocks = 0,  // prefill Q blocks (sum over Q-block-kernel sequences)
+  kHdrNumDecodes = 1,    // sequences routed to the decode kernel K2
+  kHdrTotalChunks = 2,   // decode segments ("chunks") over all decode sequences
+  kHdrBlockQ = 3,        // BLOCK_Q used for Q-block packing
+  kHdrChunkBlocks = 4,   // decode segment length cap, in KV blocks
+  kHdrPrefillCounter = 5,  // dynamic work counters (reset by K5)
+  kHdrDecodeCounter = 6,
+  kHdrWords = 64
+};
+
+struct Params {
+  // tensors
+  const void* q;
+  const void* k;
+  const void* v;
+  void* out;
+  const int32_t* block_table;
+  const int32_t* cu_seqlens_q;
+  const int32_t* seq_lens;
+  // sizes
+  int32_t B, T, Hq, Hkv, G, D, bs, num_blocks;
+  int32_t dtype;          // 0 fp32, 1 bf16 (pattn_dtype_t)
+  int32_t block_q;        // query tokens per Q block
+  int32_t HG;             // decode head groups of 8 per KV head = ceil(G/8)
+  int32_t max_chunks;     // capacity of the partial buffers, in chunks
+  int32_t decode_to_k2;   // 1: q_b == 1 sequences go to the decode kernel
+  int32_t split_mode;     // 0 planner, 1 no split, 2 force split
+  int32_t target_items;   // decode: desired number of (chunk, kv head, head group) items
+  int32_t min_chunk_blocks;
+  int32_t num_sms;
+  int32_t kv_tok_inner;   // TMA dim order: 1 -> (d, slot, kvh, blk) [HND], 0 -> (d, kvh, slot, blk) [NHD]
+  // strides (elements)
+  int64_t q_st_tok, q_st_head;
+  int64_t kv_st_blk, kv_st_tok, kv_st_head;
+  int64_t bt_stride;
+  int64_t o_st_tok, o_st_head;
+  float scale;       // softmax scale (Eq. 1)
+  float scale_log2;  // scale * log2(e)
+  // workspace
+  int32_t* hdr;       // [kHdrWords]
+  int32_t* cu_qb;     // [B+1]
+  int32_t* cu_ch;     // [B+1]
+  float* part_m;      // [max_chunks][Hq]   (log2 domain: max of scale*log2e*s)
+  float* part_l;      // [max_chunks][Hq]
+  float* part_acc;    // [max_chunks][Hq][D]
+};
+
+}  // namespace pattn

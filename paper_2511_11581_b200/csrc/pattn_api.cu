@@ -1,0 +1,524 @@
+// pattn_api.cu -- the libpattn C ABI (include/pattn.h): validation, the host planner
+// (H1: kernel routing, BLOCK_Q, segment policy, grids), TMA descriptors (H2) and the
+// launch sequence K5 -> {K1 | K4} -> K2 -> K3 on the caller's stream(s).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+
+#include "kernels.h"
+#include "params.h"
+#include "pattn.h"
+
+using namespace pattn;
+
+namespace {
+
+constexpr int32_t kVersion = 100;  // 0.1.0
+
+struct DeviceInfo {
+  int sms = 0;
+  size_t max_smem = 0;
+  bool ok = false;
+};
+
+DeviceInfo device_info() {
+  static std::mutex mu;
+  static DeviceInfo cache[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return DeviceInfo{};
+  std::lock_guard<std::mutex> g(mu);
+  if (!cache[dev].ok) {
+    int sms = 0, smem = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return DeviceInfo{};
+    if (cudaDeviceGetAttribute(&smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
+      return DeviceInfo{};
+    cache[dev].sms = sms;
+    cache[dev].max_smem = (size_t)smem;
+    cache[dev].ok = true;
+  }
+  return cache[dev];
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static std::once_flag once;
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return (v && *v) ? atoi(v) : dflt;
+}
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+bool aligned16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15u) == 0; }
+
+struct Plan {
+  bool use_k1 = false, use_k2 = false, use_k4 = false;
+  int block_q = 1, HG = 1, rpw = 8;
+  int target_items = 0, min_chunk = 1, split_mode = 0, max_chunks = 0;
+  int num_sms = 148;
+  size_t max_smem = 0;
+  size_t off_hdr = 0, off_cuqb = 0, off_cuch = 0, off_pm = 0, off_pl = 0, off_pacc = 0, total = 0;
+  int k4_grid = 1;
+  DecodeLaunch dl{};
+  PrefillLaunch pl{};
+  bool kv_tok_inner = false;
+};
+
+pattn_status_t check_problem(const pattn_problem_t* p) {
+  if (!p) return PATTN_ERR_INVALID_ARG;
+  if (p->num_seqs <= 0) return PATTN_ERR_EMPTY_BATCH;
+  if (p->num_tokens < 0 || p->num_q_heads <= 0 || p->num_kv_heads <= 0 || p->block_size <= 0 ||
+      p->num_blocks <= 0 || p->max_blocks_per_seq <= 0)
+    return PATTN_ERR_INVALID_ARG;
+  if (p->num_q_heads % p->num_kv_heads != 0) return PATTN_ERR_INVALID_ARG;
+  if (p->head_dim != 64 && p->head_dim != 128) return PATTN_ERR_UNSUPPORTED;
+  if (p->dtype != PATTN_DTYPE_F32 && p->dtype != PATTN_DTYPE_BF16) return PATTN_ERR_UNSUPPORTED;
+  if (p->num_q_heads / p->num_kv_heads > 64) return PATTN_ERR_UNSUPPORTED;
+  if (p->q_stride_tok <= 0 || p->q_stride_head <= 0 || p->kv_stride_blk <= 0 || p->kv_stride_tok <= 0 ||
+      p->kv_stride_head <= 0 || p->bt_stride < p->max_blocks_per_seq || p->o_stride_tok <= 0 ||
+      p->o_stride_head <= 0)
+    return PATTN_ERR_INVALID_ARG;
+  return PATTN_OK;
+}
+
+void fill_params(const pattn_problem_t* p, const Plan& pl, Params* k) {
+  memset(k, 0, sizeof(*k));
+  k->B = p->num_seqs;
+  k->T = p->num_tokens;
+  k->Hq = p->num_q_heads;
+  k->Hkv = p->num_kv_heads;
+  k->G = p->num_q_heads / p->num_kv_heads;
+  k->D = p->head_dim;
+  k->bs = p->block_size;
+  k->num_blocks = p->num_blocks;
+  k->dtype = p->dtype;
+  k->block_q = pl.block_q;
+  k->HG = pl.HG;
+  k->max_chunks = pl.max_chunks;
+  k->decode_to_k2 = pl.use_k2 ? 1 : 0;
+  k->split_mode = pl.split_mode;
+  k->target_items = pl.target_items;
+  k->min_chunk_blocks = pl.min_chunk;
+  k->num_sms = pl.num_sms;
+  k->kv_tok_inner = pl.kv_tok_inner ? 1 : 0;
+  k->q_st_tok = p->q_stride_tok;
+  k->q_st_head = p->q_stride_head;
+  k->kv_st_blk = p->kv_stride_blk;
+  k->kv_st_tok = p->kv_stride_tok;
+  k->kv_st_head = p->kv_stride_head;
+  k->bt_stride = p->bt_stride;
+  k->o_st_tok = p->o_stride_tok;
+  k->o_st_head = p->o_stride_head;
+}
+
+// H1 planner.  Pure host arithmetic on host-visible sizes (no device reads).
+pattn_status_t make_plan(const pattn_problem_t* p, const void* q, const void* kc, const void* vc, const void* out,
+                         Plan* pl) {
+  pattn_status_t st = check_problem(p);
+  if (st != PATTN_OK) return st;
+  DeviceInfo di = device_info();
+  pl->num_sms = di.ok ? di.sms : 148;
+  pl->max_smem = di.ok ? di.max_smem : 227 * 1024;
+  const int G = p->num_q_heads / p->num_kv_heads;
+  const int D = p->head_dim;
+  const bool bf16 = p->dtype == PATTN_DTYPE_BF16;
+  const bool generic = (p->flags & PATTN_FLAG_FORCE_GENERIC) != 0;
+  pl->HG = (G + 7) / 8;
+  pl->kv_tok_inner = p->kv_stride_tok < p->kv_stride_head;
+
+  // K2 (TMA ring) requirements: bf16, bs multiple of 16 (mma key tiles) and <= 256 (TMA box),
+  // 16-byte aligned rows and strides, dense head_dim.
+  const bool tma_ok = (p->kv_stride_blk % 8 == 0) && (p->kv_stride_tok % 8 == 0) && (p->kv_stride_head % 8 == 0) &&
+                      (kc == nullptr || aligned16(kc)) && (vc == nullptr || aligned16(vc));
+  const bool q_ok = (p->q_stride_tok % 8 == 0) && (p->q_stride_head % 8 == 0) && (q == nullptr || aligned16(q));
+  const bool o_ok = (p->o_stride_tok % 8 == 0) && (p->o_stride_head % 8 == 0) && (out == nullptr || aligned16(out));
+  pl->use_k2 = bf16 && !generic && p->block_size % 16 == 0 && p->block_size <= 256 && tma_ok && q_ok && o_ok;
+
+  Params probe;
+  fill_params(p, *pl, &probe);
+  pl->use_k1 = bf16 && !generic && tma_ok && q_ok && o_ok && prefill_supported(probe);
+  const int max_q = p->max_query_len > 0 ? p->max_query_len : p->num_tokens;
+  const bool maybe_prefill = max_q > 1 || !pl->use_k2;
+  if (pl->use_k1) {
+    pl->block_q = std::max(1, 128 / G);
+    pl->use_k1 = maybe_prefill;
+  } else {
+    pl->block_q = G <= 32 ? std::max(1, 32 / G) : 1;
+    pl->use_k4 = maybe_prefill;
+  }
+  const int bm = pl->block_q * G;
+  pl->rpw = bm <= 32 ? 8 : 16;
+
+  // decode segment policy (parallel tiled softmax): ~8 items per SM by default
+  if (p->flags & PATTN_FLAG_NO_SPLIT) {
+    pl->split_mode = 1;
+    pl->target_items = 1;
+    pl->min_chunk = 1;
+  } else if (p->flags & PATTN_FLAG_FORCE_SPLIT) {
+    pl->split_mode = 2;
+    pl->target_items = pl->num_sms * 64;
+    pl->min_chunk = 1;
+  } else {
+    pl->target_items = env_int("PATTN_TARGET_ITEMS", pl->num_sms * 8);
+    pl->min_chunk = env_int("PATTN_MIN_CHUNK_BLOCKS", std::max(1, 256 / p->block_size));
+  }
+  if (pl->target_items < 1) pl->target_items = 1;
+  if (pl->min_chunk < 1) pl->min_chunk = 1;
+  const long long units = (long long)p->num_kv_heads * pl->HG;
+  pl->max_chunks = pl->use_k2 ? (int)(p->num_seqs + (pl->target_items + units - 1) / units + 1) : 0;
+
+  // workspace layout
+  size_t off = 0;
+  pl->off_hdr = off;
+  off = align256(off + kHdrWords * sizeof(int32_t));
+  pl->off_cuqb = off;
+  off = align256(off + (size_t)(p->num_seqs + 1) * sizeof(int32_t));
+  pl->off_cuch = off;
+  off = align256(off + (size_t)(p->num_seqs + 1) * sizeof(int32_t));
+  const size_t rows = (size_t)pl->max_chunks * p->num_q_heads;
+  pl->off_pm = off;
+  off = align256(off + rows * sizeof(float));
+  pl->off_pl = off;
+  off = align256(off + rows * sizeof(float));
+  pl->off_pacc = off;
+  off = align256(off + rows * (size_t)D * sizeof(float));
+  pl->total = off;
+
+  // grids
+  if (pl->use_k4) {
+    const int ctas_per_sm = 4;
+    const long long max_items = (long long)std::max(1, p->num_tokens) * p->num_kv_heads;
+    pl->k4_grid = (int)std::min<long long>(max_items, (long long)pl->num_sms * ctas_per_sm);
+    if (pl->k4_grid < 1) pl->k4_grid = 1;
+  }
+  fill_params(p, *pl, &probe);
+  if (pl->use_k2) pl->dl = plan_decode(probe, pl->num_sms, pl->max_smem);
+  if (pl->use_k1) pl->pl = plan_prefill(probe, pl->num_sms);
+  return PATTN_OK;
+}
+
+// H2: 4-D tensor map over one paged cache: dims ordered by stride so they nest.
+bool encode_kv_map(CUtensorMap* tm, const pattn_problem_t* p, const void* base, bool tok_inner) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[4];
+  cuuint64_t strides[3];
+  cuuint32_t box[4];
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  dims[0] = (cuuint64_t)p->head_dim;
+  if (tok_inner) {
+    dims[1] = (cuuint64_t)p->block_size;
+    dims[2] = (cuuint64_t)p->num_kv_heads;
+    strides[0] = (cuuint64_t)p->kv_stride_tok * 2;
+    strides[1] = (cuuint64_t)p->kv_stride_head * 2;
+    box[1] = (cuuint32_t)p->block_size;
+    box[2] = 1;
+  } else {
+    dims[1] = (cuuint64_t)p->num_kv_heads;
+    dims[2] = (cuuint64_t)p->block_size;
+    strides[0] = (cuuint64_t)p->kv_stride_head * 2;
+    strides[1] = (cuuint64_t)p->kv_stride_tok * 2;
+    box[1] = 1;
+    box[2] = (cuuint32_t)p->block_size;
+  }
+  dims[3] = (cuuint64_t)p->num_blocks;
+  strides[2] = (cuuint64_t)p->kv_stride_blk * 2;
+  box[0] = 64;
+  box[3] = 1;
+  CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// Q viewed as [T][Hkv][G][D]: box {64 d, G heads, BLOCK_Q tokens} -> BLOCK_M = BLOCK_Q*G rows
+// of 128 B, token-major / head-minor (reading R8).
+bool encode_q_map(CUtensorMap* tm, const pattn_problem_t* p, const void* q, int block_q) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  const int G = p->num_q_heads / p->num_kv_heads;
+  cuuint64_t dims[4] = {(cuuint64_t)p->head_dim, (cuuint64_t)G, (cuuint64_t)p->num_kv_heads,
+                        (cuuint64_t)std::max(1, p->num_tokens)};
+  cuuint64_t strides[3] = {(cuuint64_t)p->q_stride_head * 2, (cuuint64_t)p->q_stride_head * 2 * G,
+                           (cuuint64_t)p->q_stride_tok * 2};
+  cuuint32_t box[4] = {64, (cuuint32_t)G, 1, (cuuint32_t)block_q};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(q), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+struct EventRec {
+  const pattn_exec_opts_t* o;
+  void rec(int idx, cudaStream_t s) const {
+    if (o && o->events[idx]) cudaEventRecord(static_cast<cudaEvent_t>(o->events[idx]), s);
+  }
+};
+
+pattn_status_t run(const pattn_problem_t* p, const void* q, const void* k_cache, const void* v_cache,
+                   const int32_t* block_table, const int32_t* cu_seqlens_q, const int32_t* seq_lens, float scale,
+                   void* out, void* workspace, size_t workspace_bytes, void* stream_v,
+                   const pattn_exec_opts_t* opts, bool metadata_only) {
+  Plan pl;
+  pattn_status_t st = make_plan(p, q, k_cache, v_cache, out, &pl);
+  if (st != PATTN_OK) return st;
+  if (!q || !k_cache || !v_cache || !block_table || !cu_seqlens_q || !seq_lens || !out || !workspace)
+    return PATTN_ERR_INVALID_ARG;
+  if ((reinterpret_cast<uintptr_t>(workspace) & 255u) != 0) return PATTN_ERR_INVALID_ARG;
+  if (workspace_bytes < pl.total) return PATTN_ERR_WORKSPACE_TOO_SMALL;
+  if (!(scale == scale) || scale > 3.0e38f || scale < -3.0e38f) return PATTN_ERR_INVALID_ARG;
+
+  cudaStream_t s1 = static_cast<cudaStream_t>(stream_v);
+  cudaStream_t s2 = (opts && opts->stream2 && !(p->flags & PATTN_FLAG_SERIAL)) ? static_cast<cudaStream_t>(opts->stream2)
+                                                                               : s1;
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  Params k;
+  fill_params(p, pl, &k);
+  k.q = q;
+  k.k = k_cache;
+  k.v = v_cache;
+  k.out = out;
+  k.block_table = block_table;
+  k.cu_seqlens_q = cu_seqlens_q;
+  k.seq_lens = seq_lens;
+  k.scale = scale;
+  k.scale_log2 = scale * 1.4426950408889634f;
+  k.hdr = reinterpret_cast<int32_t*>(ws + pl.off_hdr);
+  k.cu_qb = reinterpret_cast<int32_t*>(ws + pl.off_cuqb);
+  k.cu_ch = reinterpret_cast<int32_t*>(ws + pl.off_cuch);
+  k.part_m = reinterpret_cast<float*>(ws + pl.off_pm);
+  k.part_l = reinterpret_cast<float*>(ws + pl.off_pl);
+  k.part_acc = reinterpret_cast<float*>(ws + pl.off_pacc);
+
+  CUtensorMap tmK, tmV, tmQ;
+  if (!metadata_only) {
+    if (pl.use_k2 || pl.use_k1) {
+      if (!encode_kv_map(&tmK, p, k_cache, pl.kv_tok_inner) || !encode_kv_map(&tmV, p, v_cache, pl.kv_tok_inner))
+        return PATTN_ERR_UNSUPPORTED;
+    }
+    if (pl.use_k1) {
+      if (!encode_q_map(&tmQ, p, q, pl.block_q)) return PATTN_ERR_UNSUPPORTED;
+    }
+  }
+
+  EventRec ev{opts};
+  cudaError_t e;
+  ev.rec(2 * PATTN_KERNEL_METADATA, s1);
+  e = launch_metadata(k, s1);
+  ev.rec(2 * PATTN_KERNEL_METADATA + 1, s1);
+  if (e != cudaSuccess) return PATTN_ERR_CUDA;
+  if (metadata_only) return PATTN_OK;
+
+  cudaEvent_t fork = nullptr, join = nullptr;
+  const bool two = (s2 != s1) && pl.use_k2 && (pl.use_k1 || pl.use_k4);
+  if (two) {
+    cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&join, cudaEventDisableTiming);
+    cudaEventRecord(fork, s1);
+    cudaStreamWaitEvent(s2, fork, 0);
+  }
+  cudaStream_t sd = two ? s2 : s1;
+  if (pl.use_k2) {
+    ev.rec(2 * PATTN_KERNEL_DECODE, sd);
+    e = launch_decode(k, pl.dl, tmK, tmV, sd);
+    ev.rec(2 * PATTN_KERNEL_DECODE + 1, sd);
+    if (e != cudaSuccess) return PATTN_ERR_CUDA;
+    ev.rec(2 * PATTN_KERNEL_REDUCE, sd);
+    e = launch_reduce(k, sd);
+    ev.rec(2 * PATTN_KERNEL_REDUCE + 1, sd);
+    if (e != cudaSuccess) return PATTN_ERR_CUDA;
+  }
+  if (pl.use_k1) {
+    ev.rec(2 * PATTN_KERNEL_PREFILL, s1);
+    e = launch_prefill(k, pl.pl, tmQ, tmK, tmV, s1);
+    ev.rec(2 * PATTN_KERNEL_PREFILL + 1, s1);
+    if (e != cudaSuccess) return PATTN_ERR_CUDA;
+  }
+  if (pl.use_k4) {
+    ev.rec(2 * PATTN_KERNEL_GENERIC, s1);
+    e = launch_generic(k, pl.k4_grid, pl.rpw, s1);
+    ev.rec(2 * PATTN_KERNEL_GENERIC + 1, s1);
+    if (e != cudaSuccess) return PATTN_ERR_CUDA;
+  }
+  if (two) {
+    cudaEventRecord(join, s2);
+    cudaStreamWaitEvent(s1, join, 0);
+    cudaEventDestroy(fork);
+    cudaEventDestroy(join);
+  }
+  return PATTN_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t pattn_workspace_size(const pattn_problem_t* p) {
+  Plan pl;
+  if (make_plan(p, nullptr, nullptr, nullptr, nullptr, &pl) != PATTN_OK) return 0;
+  return pl.total;
+}
+
+pattn_status_t pattn_unified_attention(const pattn_problem_t* p, const void* q, const void* k_cache,
+                                       const void* v_cache, const int32_t* block_table,
+                                       const int32_t* cu_seqlens_q, const int32_t* seq_lens, float scale,
+                                       void* out, void* workspace, size_t workspace_bytes, void* stream) {
+  return run(p, q, k_cache, v_cache, block_table, cu_seqlens_q, seq_lens, scale, out, workspace, workspace_bytes,
+             stream, nullptr, false);
+}
+
+pattn_status_t pattn_unified_attention_ex(const pattn_problem_t* p, const void* q, const void* k_cache,
+                                          const void* v_cache, const int32_t* block_table,
+                                          const int32_t* cu_seqlens_q, const int32_t* seq_lens, float scale,
+                                          void* out, void* workspace, size_t workspace_bytes, void* stream,
+                                          const pattn_exec_opts_t* opts) {
+  return run(p, q, k_cache, v_cache, block_table, cu_seqlens_q, seq_lens, scale, out, workspace, workspace_bytes,
+             stream, opts, false);
+}
+
+// ---- end-to-end (host buffers) variant
+namespace {
+struct HostIoLayout {
+  size_t base, q, bt, cu, sl, out, total;
+};
+bool hostio_layout(const pattn_problem_t* p, HostIoLayout* L) {
+  size_t base = pattn_workspace_size(p);
+  if (!base) return false;
+  const size_t esz = p->dtype == PATTN_DTYPE_F32 ? 4 : 2;
+  size_t off = align256(base);
+  L->base = base;
+  L->q = off;
+  off = align256(off + (size_t)p->num_tokens * p->num_q_heads * p->head_dim * esz);
+  L->bt = off;
+  off = align256(off + (size_t)p->num_seqs * p->bt_stride * sizeof(int32_t));
+  L->cu = off;
+  off = align256(off + (size_t)(p->num_seqs + 1) * sizeof(int32_t));
+  L->sl = off;
+  off = align256(off + (size_t)p->num_seqs * sizeof(int32_t));
+  L->out = off;
+  off = align256(off + (size_t)p->num_tokens * p->num_q_heads * p->head_dim * esz);
+  L->total = off;
+  return true;
+}
+}  // namespace
+
+size_t pattn_hostio_workspace_size(const pattn_problem_t* p) {
+  HostIoLayout L;
+  return hostio_layout(p, &L) ? L.total : 0;
+}
+
+pattn_status_t pattn_unified_attention_hostio(const pattn_problem_t* p, const void* q_host, const void* k_cache,
+                                              const void* v_cache, const int32_t* block_table_host,
+                                              const int32_t* cu_seqlens_q_host, const int32_t* seq_lens_host,
+                                              float scale, void* out_host, void* workspace, size_t workspace_bytes,
+                                              void* stream) {
+  pattn_status_t st = check_problem(p);
+  if (st != PATTN_OK) return st;
+  if (!q_host || !block_table_host || !cu_seqlens_q_host || !seq_lens_host || !out_host || !workspace)
+    return PATTN_ERR_INVALID_ARG;
+  if (p->q_stride_head != p->head_dim || p->q_stride_tok != (int64_t)p->num_q_heads * p->head_dim ||
+      p->o_stride_head != p->head_dim || p->o_stride_tok != (int64_t)p->num_q_heads * p->head_dim)
+    return PATTN_ERR_INVALID_ARG;
+  HostIoLayout L;
+  if (!hostio_layout(p, &L)) return PATTN_ERR_INVALID_ARG;
+  if (workspace_bytes < L.total) return PATTN_ERR_WORKSPACE_TOO_SMALL;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  const size_t esz = p->dtype == PATTN_DTYPE_F32 ? 4 : 2;
+  const size_t qbytes = (size_t)p->num_tokens * p->num_q_heads * p->head_dim * esz;
+  if (cudaMemcpyAsync(ws + L.q, q_host, qbytes, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+      cudaMemcpyAsync(ws + L.bt, block_table_host, (size_t)p->num_seqs * p->bt_stride * 4, cudaMemcpyHostToDevice,
+                      s) != cudaSuccess ||
+      cudaMemcpyAsync(ws + L.cu, cu_seqlens_q_host, (size_t)(p->num_seqs + 1) * 4, cudaMemcpyHostToDevice, s) !=
+          cudaSuccess ||
+      cudaMemcpyAsync(ws + L.sl, seq_lens_host, (size_t)p->num_seqs * 4, cudaMemcpyHostToDevice, s) != cudaSuccess)
+    return PATTN_ERR_CUDA;
+  st = run(p, ws + L.q, k_cache, v_cache, reinterpret_cast<int32_t*>(ws + L.bt), reinterpret_cast<int32_t*>(ws + L.cu),
+           reinterpret_cast<int32_t*>(ws + L.sl), scale, ws + L.out, workspace, L.base, stream, nullptr, false);
+  if (st != PATTN_OK) return st;
+  if (cudaMemcpyAsync(out_host, ws + L.out, qbytes, cudaMemcpyDeviceToHost, s) != cudaSuccess) return PATTN_ERR_CUDA;
+  return PATTN_OK;
+}
+
+const char* pattn_status_string(pattn_status_t s) {
+  switch (s) {
+    case PATTN_OK: return "PATTN_OK";
+    case PATTN_ERR_INVALID_ARG: return "PATTN_ERR_INVALID_ARG";
+    case PATTN_ERR_EMPTY_BATCH: return "PATTN_ERR_EMPTY_BATCH";
+    case PATTN_ERR_INVALID_SEQUENCE: return "PATTN_ERR_INVALID_SEQUENCE";
+    case PATTN_ERR_INDEX_OUT_OF_RANGE: return "PATTN_ERR_INDEX_OUT_OF_RANGE";
+    case PATTN_ERR_UNSUPPORTED: return "PATTN_ERR_UNSUPPORTED";
+    case PATTN_ERR_WORKSPACE_TOO_SMALL: return "PATTN_ERR_WORKSPACE_TOO_SMALL";
+    case PATTN_ERR_CUDA: return "PATTN_ERR_CUDA";
+  }
+  return "PATTN_ERR_UNKNOWN";
+}
+
+pattn_status_t pattn_validate_metadata_host(const pattn_problem_t* p, const int32_t* cu, const int32_t* sl,
+                                            const int32_t* bt) {
+  if (!p) return PATTN_ERR_INVALID_ARG;
+  if (p->num_seqs <= 0) return PATTN_ERR_EMPTY_BATCH;
+  if (!cu || !sl || !bt || p->block_size <= 0) return PATTN_ERR_INVALID_ARG;
+  if (cu[0] != 0 || cu[p->num_seqs] != p->num_tokens) return PATTN_ERR_INVALID_SEQUENCE;
+  for (int b = 0; b < p->num_seqs; ++b) {
+    const int64_t qb = (int64_t)cu[b + 1] - cu[b];
+    if (qb < 0 || qb > sl[b]) return PATTN_ERR_INVALID_SEQUENCE;
+    const int64_t nblk = ((int64_t)sl[b] + p->block_size - 1) / p->block_size;
+    if (nblk > p->max_blocks_per_seq) return PATTN_ERR_INDEX_OUT_OF_RANGE;
+    for (int64_t j = 0; j < nblk; ++j) {
+      const int32_t id = bt[(int64_t)b * p->bt_stride + j];
+      if (id < 0 || id >= p->num_blocks) return PATTN_ERR_INDEX_OUT_OF_RANGE;
+    }
+  }
+  return PATTN_OK;
+}
+
+pattn_status_t pattn_debug_plan(const pattn_problem_t* p, const int32_t* cu_seqlens_q, const int32_t* seq_lens,
+                                int32_t* plan_out, int32_t plan_capacity, void* workspace, size_t workspace_bytes,
+                                void* stream) {
+  if (!p || !plan_out || plan_capacity < 2 * p->num_seqs + 10) return PATTN_ERR_INVALID_ARG;
+  Plan pl;
+  pattn_status_t st = make_plan(p, nullptr, nullptr, nullptr, nullptr, &pl);
+  if (st != PATTN_OK) return st;
+  // metadata only: dummy non-null tensor pointers are never dereferenced by K5
+  const void* dummy = workspace;
+  st = run(p, dummy, dummy, dummy, cu_seqlens_q, cu_seqlens_q, seq_lens, 1.0f, workspace, workspace, workspace_bytes,
+           stream, nullptr, true);
+  if (st != PATTN_OK) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  const int B = p->num_seqs;
+  if (cudaMemcpyAsync(plan_out, ws + pl.off_hdr, 8 * sizeof(int32_t), cudaMemcpyDeviceToDevice, s) != cudaSuccess ||
+      cudaMemcpyAsync(plan_out + 8, ws + pl.off_cuqb, (B + 1) * sizeof(int32_t), cudaMemcpyDeviceToDevice, s) !=
+          cudaSuccess ||
+      cudaMemcpyAsync(plan_out + 8 + B + 1, ws + pl.off_cuch, (B + 1) * sizeof(int32_t), cudaMemcpyDeviceToDevice,
+                      s) != cudaSuccess)
+    return PATTN_ERR_CUDA;
+  return PATTN_OK;
+}
+
+int32_t pattn_planned_launches(const pattn_problem_t* p) {
+  Plan pl;
+  if (make_plan(p, nullptr, nullptr, nullptr, nullptr, &pl) != PATTN_OK) return 0;
+  return 1 + (pl.use_k1 ? 1 : 0) + (pl.use_k4 ? 1 : 0) + (pl.use_k2 ? 2 : 0);
+}
+
+int32_t pattn_version(void) { return kVersion; }
+
+}  // extern "C"

@@ -1,0 +1,340 @@
+"""Thin Python binding of libpattn (include/pattn.h) -- argument marshalling only.
+
+Every step of the attention path runs inside libpattn's CUDA kernels; this module
+only turns torch tensors into pointers, sizes and strides, keeps a cached device
+workspace, and calls the C ABI through ctypes.  There is no CPU fallback: if the
+shared library is missing, importing the call raises.
+
+Names follow north_star: unified_attention(q, k_cache, v_cache, block_table,
+cu_seqlens_q, seq_lens, scale, num_kv_heads, block_size, out).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+from typing import Optional, Sequence
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libpattn.so")
+
+PATTN_OK = 0
+STATUS = {
+    0: "PATTN_OK",
+    1: "PATTN_ERR_INVALID_ARG",
+    2: "PATTN_ERR_EMPTY_BATCH",
+    3: "PATTN_ERR_INVALID_SEQUENCE",
+    4: "PATTN_ERR_INDEX_OUT_OF_RANGE",
+    5: "PATTN_ERR_UNSUPPORTED",
+    6: "PATTN_ERR_WORKSPACE_TOO_SMALL",
+    7: "PATTN_ERR_CUDA",
+}
+DTYPE_F32, DTYPE_BF16 = 0, 1
+FLAG_FORCE_GENERIC, FLAG_NO_SPLIT, FLAG_FORCE_SPLIT, FLAG_SERIAL = 0x1, 0x2, 0x4, 0x8
+KERNEL_METADATA, KERNEL_PREFILL, KERNEL_DECODE, KERNEL_REDUCE, KERNEL_GENERIC, KERNEL_COUNT = range(6)
+KERNEL_NAMES = ["metadata", "prefill", "decode", "reduce", "generic"]
+
+
+class PattnError(RuntimeError):
+    def __init__(self, code: int, where: str):
+        super().__init__(f"{where}: {STATUS.get(code, code)}")
+        self.code = code
+
+
+class Problem(ctypes.Structure):
+    _fields_ = [
+        ("num_seqs", ctypes.c_int32),
+        ("num_tokens", ctypes.c_int32),
+        ("num_q_heads", ctypes.c_int32),
+        ("num_kv_heads", ctypes.c_int32),
+        ("head_dim", ctypes.c_int32),
+        ("block_size", ctypes.c_int32),
+        ("num_blocks", ctypes.c_int32),
+        ("max_blocks_per_seq", ctypes.c_int32),
+        ("max_query_len", ctypes.c_int32),
+        ("max_seq_len", ctypes.c_int32),
+        ("dtype", ctypes.c_int32),
+        ("flags", ctypes.c_int32),
+        ("q_stride_tok", ctypes.c_int64),
+        ("q_stride_head", ctypes.c_int64),
+        ("kv_stride_blk", ctypes.c_int64),
+        ("kv_stride_tok", ctypes.c_int64),
+        ("kv_stride_head", ctypes.c_int64),
+        ("bt_stride", ctypes.c_int64),
+        ("o_stride_tok", ctypes.c_int64),
+        ("o_stride_head", ctypes.c_int64),
+    ]
+
+
+class ExecOpts(ctypes.Structure):
+    _fields_ = [("stream2", ctypes.c_void_p), ("events", ctypes.c_void_p * (2 * KERNEL_COUNT))]
+
+
+_lib = None
+_lock = threading.Lock()
+
+EXPORTS = [
+    "pattn_workspace_size",
+    "pattn_unified_attention",
+    "pattn_unified_attention_ex",
+    "pattn_hostio_workspace_size",
+    "pattn_unified_attention_hostio",
+    "pattn_status_string",
+    "pattn_validate_metadata_host",
+    "pattn_debug_plan",
+    "pattn_planned_launches",
+    "pattn_version",
+]
+
+
+def load() -> ctypes.CDLL:
+    """Load libpattn.so (fail loudly when it has not been built)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise ImportError(f"libpattn not built: {LIB_PATH} missing (run `make` or __graft_entry__.build())")
+            lib = ctypes.CDLL(LIB_PATH)
+            P = ctypes.POINTER(Problem)
+            vp, i32p, sz = ctypes.c_void_p, ctypes.POINTER(ctypes.c_int32), ctypes.c_size_t
+            lib.pattn_workspace_size.restype = sz
+            lib.pattn_workspace_size.argtypes = [P]
+            lib.pattn_hostio_workspace_size.restype = sz
+            lib.pattn_hostio_workspace_size.argtypes = [P]
+            common = [P, vp, vp, vp, vp, vp, vp, ctypes.c_float, vp, vp, sz, vp]
+            lib.pattn_unified_attention.restype = ctypes.c_int
+            lib.pattn_unified_attention.argtypes = common
+            lib.pattn_unified_attention_ex.restype = ctypes.c_int
+            lib.pattn_unified_attention_ex.argtypes = common + [ctypes.POINTER(ExecOpts)]
+            lib.pattn_unified_attention_hostio.restype = ctypes.c_int
+            lib.pattn_unified_attention_hostio.argtypes = common
+            lib.pattn_status_string.restype = ctypes.c_char_p
+            lib.pattn_status_string.argtypes = [ctypes.c_int]
+            lib.pattn_validate_metadata_host.restype = ctypes.c_int
+            lib.pattn_validate_metadata_host.argtypes = [P, i32p, i32p, i32p]
+            lib.pattn_debug_plan.restype = ctypes.c_int
+            lib.pattn_debug_plan.argtypes = [P, vp, vp, vp, ctypes.c_int32, vp, sz, vp]
+            lib.pattn_planned_launches.restype = ctypes.c_int32
+            lib.pattn_planned_launches.argtypes = [P]
+            lib.pattn_version.restype = ctypes.c_int32
+            _lib = lib
+    return _lib
+
+
+def _check(code: int, where: str):
+    if code != PATTN_OK:
+        raise PattnError(code, where)
+
+
+def _dtype_code(t: torch.Tensor) -> int:
+    if t.dtype == torch.float32:
+        return DTYPE_F32
+    if t.dtype == torch.bfloat16:
+        return DTYPE_BF16
+    raise PattnError(5, f"dtype {t.dtype}")
+
+
+def make_problem(
+    q: torch.Tensor,
+    k_cache: torch.Tensor,
+    num_kv_heads: int,
+    block_size: int,
+    block_table: torch.Tensor,
+    num_seqs: int,
+    out: Optional[torch.Tensor] = None,
+    kv_layout: str = "NHD",
+    max_query_len: Optional[int] = None,
+    max_seq_len: Optional[int] = None,
+    flags: int = 0,
+) -> Problem:
+    """Sizes and element strides from tensor shapes (host-known; no device reads)."""
+    T, Hq, D = q.shape
+    if kv_layout == "NHD":
+        nb, bs, hkv, d = k_cache.shape
+        s_blk, s_tok, s_head, s_d = k_cache.stride()
+    elif kv_layout == "HND":
+        nb, hkv, bs, d = k_cache.shape
+        s_blk, s_head, s_tok, s_d = k_cache.stride()
+    else:
+        raise ValueError(kv_layout)
+    if bs != block_size or hkv != num_kv_heads or d != D or s_d != 1 or q.stride(2) != 1:
+        raise PattnError(1, "shape/stride mismatch")
+    o = out if out is not None else q
+    p = Problem()
+    p.num_seqs = num_seqs
+    p.num_tokens = T
+    p.num_q_heads = Hq
+    p.num_kv_heads = num_kv_heads
+    p.head_dim = D
+    p.block_size = block_size
+    p.num_blocks = nb
+    p.max_blocks_per_seq = block_table.shape[1]
+    p.max_query_len = int(max_query_len) if max_query_len is not None else 0
+    p.max_seq_len = int(max_seq_len) if max_seq_len is not None else 0
+    p.dtype = _dtype_code(q)
+    p.flags = flags
+    p.q_stride_tok, p.q_stride_head = q.stride(0), q.stride(1)
+    p.kv_stride_blk, p.kv_stride_tok, p.kv_stride_head = s_blk, s_tok, s_head
+    p.bt_stride = block_table.stride(0)
+    p.o_stride_tok, p.o_stride_head = o.stride(0), o.stride(1)
+    return p
+
+
+class _Workspace:
+    """Per-device cached workspace (grows, never shrinks)."""
+
+    def __init__(self):
+        self.buf = {}
+
+    def get(self, nbytes: int, device: torch.device) -> torch.Tensor:
+        key = device.index if device.index is not None else torch.cuda.current_device()
+        b = self.buf.get(key)
+        if b is None or b.numel() < nbytes:
+            b = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
+            self.buf[key] = b
+        return b
+
+
+_ws = _Workspace()
+
+
+def workspace_size(problem: Problem) -> int:
+    n = load().pattn_workspace_size(ctypes.byref(problem))
+    if n == 0:
+        raise PattnError(1, "pattn_workspace_size")
+    return int(n)
+
+
+def unified_attention(
+    q: torch.Tensor,
+    k_cache: torch.Tensor,
+    v_cache: torch.Tensor,
+    block_table: torch.Tensor,
+    cu_seqlens_q: torch.Tensor,
+    seq_lens: torch.Tensor,
+    scale: float,
+    num_kv_heads: int,
+    block_size: int,
+    out: Optional[torch.Tensor] = None,
+    *,
+    kv_layout: str = "NHD",
+    max_query_len: Optional[int] = None,
+    max_seq_len: Optional[int] = None,
+    flags: int = 0,
+    workspace: Optional[torch.Tensor] = None,
+    stream: Optional[torch.cuda.Stream] = None,
+    stream2: Optional[torch.cuda.Stream] = None,
+    events: Optional[Sequence[Optional[torch.cuda.Event]]] = None,
+) -> torch.Tensor:
+    """Unified paged attention over a mixed prefill/decode batch (see include/pattn.h).
+
+    q [T, Hq, D]; k_cache / v_cache [num_blocks, block_size, Hkv, D] ("NHD") or
+    [num_blocks, Hkv, block_size, D] ("HND"); block_table int32 [B, max_blocks];
+    cu_seqlens_q int32 [B+1]; seq_lens int32 [B] (context + query).  All on one CUDA
+    device.  Enqueued on `stream` (default: current); returns `out` without syncing.
+    """
+    lib = load()
+    if out is None:
+        out = torch.empty_like(q)
+    B = seq_lens.shape[0]
+    p = make_problem(q, k_cache, num_kv_heads, block_size, block_table, B, out, kv_layout, max_query_len,
+                     max_seq_len, flags)
+    need = workspace_size(p)
+    ws = workspace if workspace is not None else _ws.get(need, q.device)
+    s = stream if stream is not None else torch.cuda.current_stream(q.device)
+    args = (
+        ctypes.byref(p), q.data_ptr(), k_cache.data_ptr(), v_cache.data_ptr(), block_table.data_ptr(),
+        cu_seqlens_q.data_ptr(), seq_lens.data_ptr(), ctypes.c_float(scale), out.data_ptr(), ws.data_ptr(),
+        ws.numel(), s.cuda_stream,
+    )
+    if stream2 is None and events is None:
+        _check(lib.pattn_unified_attention(*args), "pattn_unified_attention")
+    else:
+        o = ExecOpts()
+        o.stream2 = stream2.cuda_stream if stream2 is not None else None
+        if events is not None:
+            for i, e in enumerate(events):
+                o.events[i] = e.cuda_event if e is not None else None
+        _check(lib.pattn_unified_attention_ex(*args, ctypes.byref(o)), "pattn_unified_attention_ex")
+    return out
+
+
+def unified_attention_hostio(
+    q_host: torch.Tensor,
+    k_cache: torch.Tensor,
+    v_cache: torch.Tensor,
+    block_table_host: torch.Tensor,
+    cu_seqlens_q_host: torch.Tensor,
+    seq_lens_host: torch.Tensor,
+    scale: float,
+    num_kv_heads: int,
+    block_size: int,
+    out_host: torch.Tensor,
+    *,
+    kv_layout: str = "NHD",
+    max_query_len: Optional[int] = None,
+    max_seq_len: Optional[int] = None,
+    flags: int = 0,
+    workspace: Optional[torch.Tensor] = None,
+    stream: Optional[torch.cuda.Stream] = None,
+) -> torch.Tensor:
+    """End-to-end call: q / metadata / out are (pinned) HOST tensors, the caches are on the device.
+    The H2D copies, the attention and the D2H copy are enqueued on `stream`; sync before reading out_host."""
+    lib = load()
+    B = seq_lens_host.shape[0]
+    p = make_problem(q_host, k_cache, num_kv_heads, block_size, block_table_host, B, out_host, kv_layout,
+                     max_query_len, max_seq_len, flags)
+    need = int(lib.pattn_hostio_workspace_size(ctypes.byref(p)))
+    if need == 0:
+        raise PattnError(1, "pattn_hostio_workspace_size")
+    ws = workspace if workspace is not None else _ws.get(need, k_cache.device)
+    s = stream if stream is not None else torch.cuda.current_stream(k_cache.device)
+    _check(
+        lib.pattn_unified_attention_hostio(
+            ctypes.byref(p), q_host.data_ptr(), k_cache.data_ptr(), v_cache.data_ptr(), block_table_host.data_ptr(),
+            cu_seqlens_q_host.data_ptr(), seq_lens_host.data_ptr(), ctypes.c_float(scale), out_host.data_ptr(),
+            ws.data_ptr(), ws.numel(), s.cuda_stream,
+        ),
+        "pattn_unified_attention_hostio",
+    )
+    return out_host
+
+
+def debug_plan(problem: Problem, cu_seqlens_q: torch.Tensor, seq_lens: torch.Tensor) -> torch.Tensor:
+    """Run only the metadata kernel K5 and return its plan (int32 device tensor, layout in pattn.h)."""
+    lib = load()
+    B = problem.num_seqs
+    cap = 2 * B + 10
+    plan = torch.full((cap,), -7, dtype=torch.int32, device=cu_seqlens_q.device)
+    need = workspace_size(problem)
+    ws = _ws.get(need, cu_seqlens_q.device)
+    s = torch.cuda.current_stream(cu_seqlens_q.device)
+    _check(
+        lib.pattn_debug_plan(ctypes.byref(problem), cu_seqlens_q.data_ptr(), seq_lens.data_ptr(), plan.data_ptr(), cap,
+                             ws.data_ptr(), ws.numel(), s.cuda_stream),
+        "pattn_debug_plan",
+    )
+    return plan
+
+
+def validate_metadata_host(problem: Problem, cu_seqlens_q, seq_lens, block_table) -> int:
+    """Host-side metadata validation (SPEC error taxonomy); inputs are CPU int32 tensors/arrays."""
+    import numpy as np
+
+    lib = load()
+    cu = np.ascontiguousarray(cu_seqlens_q, np.int32)
+    sl = np.ascontiguousarray(seq_lens, np.int32)
+    bt = np.ascontiguousarray(block_table, np.int32)
+    i32p = ctypes.POINTER(ctypes.c_int32)
+    return int(lib.pattn_validate_metadata_host(ctypes.byref(problem), cu.ctypes.data_as(i32p),
+                                                sl.ctypes.data_as(i32p), bt.ctypes.data_as(i32p)))
+
+
+def planned_launches(problem: Problem) -> int:
+    return int(load().pattn_planned_launches(ctypes.byref(problem)))
+
+
+def version() -> int:
+    return int(load().pattn_version())

@@ -1,0 +1,229 @@
+"""GPU parity: libpattn (through its C ABI) vs the fp64 oracle, element by element, on the
+same seeded inputs (workloads/).  Tolerances from north_star: bf16 |err| <= 1e-2 + 1e-2|ref|,
+fp32 |err| <= 1e-5 + 1e-5|ref|; indexing bit-exact (needle tests, debug_plan)."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import attention as O
+from oracle import metadata as M
+from workloads import CONFIGS, Workload, generate
+from workloads.gen import random_workload
+
+from gpu_helpers import DeviceBatch, assert_close, out_f64
+
+pytestmark = pytest.mark.gpu
+
+P = None
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    global P
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2511_11581_b200 import pattn
+
+    pattn.load()
+    P = pattn
+
+
+def _check(batch, flags=0, what=""):
+    ref = O.batch_attention(batch)
+    db = DeviceBatch(batch)
+    gpu = out_f64(db.run(flags=flags))
+    return assert_close(gpu, ref, batch.dtype, what or batch.workload.name)
+
+
+# ---------------------------------------------------------------- config 1 (fp32)
+@pytest.mark.parametrize("layout", ["NHD", "HND"])
+def test_config1_fp32(layout):
+    batch = generate(CONFIGS["c1_tiny"], seed=1001, layout=layout)
+    _check(batch)
+
+
+def test_config1_as_bf16_all_paths():
+    w = CONFIGS["c1_tiny"]
+    wb = Workload("c1_bf16", w.seqs, w.num_q_heads, w.num_kv_heads, w.head_dim, w.block_size, "bf16")
+    batch = generate(wb, seed=1001)
+    for flags in (0, P.FLAG_FORCE_GENERIC, P.FLAG_NO_SPLIT, P.FLAG_FORCE_SPLIT):
+        _check(batch, flags, f"c1 bf16 flags={flags}")
+
+
+# ---------------------------------------------------------------- random mixed batches
+CASES = [
+    # heads, D, bs, dtype, layout, dist
+    ((32, 8), 128, 16, "bf16", "NHD", "uniform"),
+    ((32, 8), 128, 16, "bf16", "NHD", "peaked"),
+    ((64, 8), 128, 16, "bf16", "HND", "peaked"),
+    ((16, 1), 128, 32, "bf16", "NHD", "peaked"),
+    ((8, 8), 64, 16, "bf16", "NHD", "peaked"),
+    ((12, 2), 128, 80, "bf16", "NHD", "peaked"),   # bs 80 (hybrid-model block size)
+    ((4, 1), 64, 7, "bf16", "HND", "peaked"),      # bs not a multiple of 16 -> generic path
+    ((32, 8), 128, 16, "f32", "NHD", "peaked"),
+    ((16, 1), 64, 5, "f32", "HND", "uniform"),
+    ((128, 2), 128, 16, "bf16", "NHD", "peaked"),  # G = 64
+]
+
+
+@pytest.mark.parametrize("case", range(len(CASES)))
+@pytest.mark.parametrize("seed", [0, 1])
+def test_random_mixed(case, seed):
+    heads, D, bs, dt, layout, dist = CASES[case]
+    rng = np.random.default_rng(1000 * case + seed)
+    w = random_workload(rng, heads, D, bs, dt, max_seqs=6, max_len=700, decode_share=0.5)
+    batch = generate(w, seed=seed, dist=dist, layout=layout)
+    _check(batch, 0, f"case {case} {w.seqs}")
+    if dt == "bf16":
+        _check(batch, P.FLAG_FORCE_SPLIT, f"case {case} force-split")
+
+
+@pytest.mark.parametrize("flags", [0, 0x1, 0x2, 0x4])
+def test_long_decode_split(flags):
+    w = Workload("longdec", ((5000, 1), (3000, 1), (17, 1), (0, 1), (1, 1)), 64, 8, 128, 16, "bf16")
+    batch = generate(w, seed=5, dist="peaked")
+    _check(batch, flags, f"long decode flags={flags}")
+
+
+def test_chunked_prefill_and_empty_sequences():
+    w = Workload("chunked", ((300, 40), (0, 0), (77, 1), (5, 129), (0, 0), (0, 33)), 32, 8, 128, 16, "bf16")
+    batch = generate(w, seed=6, dist="peaked")
+    _check(batch, 0, "chunked")
+
+
+# ---------------------------------------------------------------- bit-exact indexing
+@pytest.mark.parametrize("flags", [0, 0x1, 0x4])
+def test_needle_bit_exact(flags):
+    w = Workload("needle", ((700, 1), (0, 50), (1500, 1), (40, 20), (33, 1)), 32, 8, 128, 16, "bf16")
+    batch = generate(w, seed=7, dist="needle")
+    db = DeviceBatch(batch)
+    out = db.run(flags=flags).cpu()
+    v = O.widen(batch.v_cache)
+    for b in range(w.num_seqs):
+        s, e = int(batch.cu_seqlens_q[b]), int(batch.cu_seqlens_q[b + 1])
+        for g in range(w.num_kv_heads):
+            t = int(batch.needle_pos[b, g])
+            row = torch.from_numpy(v[batch.block_table[b, t // 16], t % 16, g]).to(torch.bfloat16)
+            for h in range(g * 4, g * 4 + 4):
+                got = out[s:e, h]
+                assert torch.equal(got, row.expand_as(got)), (b, g, h, t)
+
+
+def test_needle_sweep_positions_decode():
+    # needle at every block boundary class of a split decode sequence: first/last slot, segment edges
+    L = 4097
+    for t in (0, 15, 16, 2047, 2048, 4095, 4096):
+        w = Workload("nsweep", ((L - 1, 1),), 32, 8, 128, 16, "bf16")
+        batch = generate(w, seed=8, dist="needle", needle_pos=[[t] * 8])
+        out = DeviceBatch(batch).run(flags=0x4).cpu()
+        v = O.widen(batch.v_cache)
+        row = torch.from_numpy(v[batch.block_table[0, t // 16], t % 16, 3]).to(torch.bfloat16)
+        assert torch.equal(out[0, 12], row), t
+
+
+def test_debug_plan_bit_exact():
+    rng = np.random.default_rng(9)
+    for trial in range(10):
+        w = random_workload(rng, (32, 8), 128, 16, "bf16", max_seqs=40, max_len=3000, decode_share=0.6)
+        batch = generate(w, seed=trial, poison=False)
+        db = DeviceBatch(batch)
+        for flags in (0, P.FLAG_FORCE_GENERIC, P.FLAG_FORCE_SPLIT):
+            prob = P.make_problem(db.q, db.k, w.num_kv_heads, w.block_size, db.bt, w.num_seqs, flags=flags)
+            plan = P.debug_plan(prob, db.cu, db.sl).cpu().numpy()
+            B = w.num_seqs
+            block_q = int(plan[3])
+            generic = bool(flags & P.FLAG_FORCE_GENERIC)
+            qlens = np.diff(batch.cu_seqlens_q)
+            dec = (qlens == 1) & (not generic)
+            # Q-block kernel sequences: everything not routed to the decode kernel
+            cu_qb_ref = M.build_batch_meta(np.concatenate([[0], np.cumsum(np.where(dec, 0, qlens))]),
+                                           np.where(dec, 0, batch.seq_lens), block_q)["cu_q_blocks"]
+            assert plan[8:8 + B + 1].tolist() == cu_qb_ref.tolist()
+            assert plan[0] == cu_qb_ref[-1]
+            assert plan[1] == int(dec.sum())
+            cu_ch = plan[8 + B + 1: 8 + 2 * B + 2]
+            nch = np.diff(cu_ch)
+            C = int(plan[4])
+            nblk = (batch.seq_lens + 15) // 16
+            exp = np.where(dec, -(-nblk // C), 0)
+            assert nch.tolist() == exp.tolist()
+            assert plan[2] == cu_ch[-1]
+
+
+# ---------------------------------------------------------------- robustness
+def test_poison_canary_and_determinism():
+    w = Workload("canary", ((900, 1), (0, 64), (20, 9), (4000, 1)), 32, 8, 128, 16, "bf16")
+    batch = generate(w, seed=10, dist="peaked", poison=True)
+    db = DeviceBatch(batch)
+    T, Hq, D = db.q.shape
+    big = torch.full((T + 3, Hq, D), 1234.5, dtype=torch.bfloat16, device="cuda")
+    o1 = db.run(out=big[:T]).clone()
+    assert torch.all(big[T:] == 1234.5)
+    assert torch.isfinite(o1.float()).all()
+    o2 = db.run()
+    assert torch.equal(o1, o2)
+    ref = O.batch_attention(batch)
+    assert_close(out_f64(o1), ref, "bf16", "canary")
+
+
+def test_hostio_equals_device_path():
+    w = Workload("hostio", ((100, 1), (0, 48), (2000, 1)), 32, 8, 128, 16, "bf16")
+    batch = generate(w, seed=11, dist="peaked")
+    db = DeviceBatch(batch)
+    dev = db.run().cpu()
+    q_h = db.q.cpu().pin_memory()
+    out_h = torch.empty_like(q_h).pin_memory()
+    P.unified_attention_hostio(q_h, db.k, db.v, db.bt.cpu().pin_memory(), db.cu.cpu().pin_memory(),
+                               db.sl.cpu().pin_memory(), w.scale, w.num_kv_heads, w.block_size, out_h,
+                               max_query_len=48, max_seq_len=2001)
+    torch.cuda.synchronize()
+    assert torch.equal(out_h, dev)
+
+
+def test_two_stream_equals_serial():
+    w = Workload("streams", tuple([(0, 200)] * 2 + [(1000, 1)] * 6), 32, 8, 128, 16, "bf16")
+    batch = generate(w, seed=12, dist="peaked")
+    db = DeviceBatch(batch)
+    a = db.run().clone()
+    s2 = torch.cuda.Stream()
+    b = db.run(stream2=s2)
+    assert torch.equal(a, b)
+
+
+def test_error_codes():
+    w = CONFIGS["c1_tiny"]
+    batch = generate(w, seed=13)
+    db = DeviceBatch(batch)
+    with pytest.raises(P.PattnError) as ei:
+        P.unified_attention(db.q, db.k, db.v, db.bt, db.cu, db.sl, w.scale, w.num_kv_heads, w.block_size,
+                            workspace=torch.empty(16, dtype=torch.uint8, device="cuda"))
+    assert ei.value.code == 6
+
+
+# ---------------------------------------------------------------- BASELINE.json full sizes (sampled rows)
+def _sample_rows(batch, n_random, rng):
+    w = batch.workload
+    rows = []
+    qlens = np.diff(batch.cu_seqlens_q)
+    for b in range(w.num_seqs):
+        s = int(batch.cu_seqlens_q[b])
+        if qlens[b] == 1:
+            rows += [s * w.num_q_heads + h for h in range(w.num_q_heads)]
+        elif qlens[b] > 1:
+            for tok in (s, s + int(qlens[b]) - 1):
+                rows += [tok * w.num_q_heads + h for h in range(w.num_q_heads)]
+    T = w.num_tokens
+    rows += rng.integers(0, T * w.num_q_heads, size=n_random).tolist()
+    return np.unique(np.array(rows, np.int64))
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["c2_decode8b", "c3_mixed8b", "c4_decode128k"])
+def test_full_size_sampled(name):
+    w = CONFIGS[name]
+    batch = generate(w, seed=2000 + list(CONFIGS).index(name), dist="peaked", poison=True)
+    db = DeviceBatch(batch)
+    out = out_f64(db.run()).reshape(-1, w.head_dim)
+    rows = _sample_rows(batch, 2000, np.random.default_rng(3))
+    ref = O.batch_attention(batch, rows=rows)
+    assert_close(out[rows], ref, w.dtype, name)
