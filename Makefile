@@ -6,7 +6,7 @@ ARCH    := -gencode arch=compute_100a,code=sm_100a
 CSRC    := paper_2511_11581_b200/csrc
 LIBDIR  := paper_2511_11581_b200/lib
 NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC,-fvisibility=hidden -Xptxas -v \
-           --expt-relaxed-constexpr -Iinclude -I$(CSRC) -DPATTN_BUILD
+           --expt-relaxed-constexpr -Iinclude -I$(CSRC) -DPATTN_BUILD $(EXTRA)
 SRCS    := $(CSRC)/pattn_api.cu $(CSRC)/k5_metadata.cu $(CSRC)/k4_generic.cu $(CSRC)/k2_decode.cu \
            $(CSRC)/k3_reduce.cu $(CSRC)/k1_prefill.cu
 OBJS    := $(patsubst $(CSRC)/%.cu,build/%.o,$(SRCS))

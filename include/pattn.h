@@ -210,6 +210,12 @@ PATTN_API pattn_status_t pattn_debug_plan(const pattn_problem_t* p, const int32_
 /* Number of kernel launches pattn_unified_attention enqueues for this problem (host-side plan). */
 PATTN_API int32_t pattn_planned_launches(const pattn_problem_t* p);
 
+/* Bit mask of the kernel kinds (1 << PATTN_KERNEL_*) pattn_unified_attention launches for this problem. */
+PATTN_API int32_t pattn_planned_kernels(const pattn_problem_t* p);
+
+/* Text of the CUDA error behind the calling thread's last PATTN_ERR_CUDA ("" if none). */
+PATTN_API const char* pattn_last_error(void);
+
 /* Library version (major*10000 + minor*100 + patch). */
 PATTN_API int32_t pattn_version(void);
 

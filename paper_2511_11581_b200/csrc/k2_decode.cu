@@ -3,46 +3,55 @@
 //
 // Work item = (decode segment c, KV head, head group of <= 8 query heads).  K5 split
 // every decode sequence into n_b contiguous, equal-length ranges of KV blocks
-// (segments); a persistent grid of one CTA per SM strides over the items (static
-// launch grid).  The Q block is the G query heads sharing the KV head
-// (GQA packing), so every K/V byte is read from HBM exactly once.
+// (segments); a persistent grid (2 CTAs per SM) strides over the items (static launch
+// grid).  The Q block is the G query heads sharing the KV head (GQA
+// packing), so every K/V byte is read from HBM exactly once.
 //
 // Memory path (the kernel is HBM-bound, arithmetic intensity G flop/byte):
-//   warp 0 (producer): walks the block table 32 entries at a time (one coalesced
-//     load, broadcast by shuffle), and for every KV block issues TMA tile loads
-//     (cp.async.bulk.tensor.4d, box {64 d, 1 head, bs slots, 1 block}, 128B swizzle)
-//     of K and V into an NST-stage shared-memory ring guarded by mbarriers.  The
-//     ring holds ~160 KB per SM in flight.
-//   warps 1..NCW (consumers): block j of the item goes to warp j % NCW.  Scores
-//     S^T[16 keys x 8 heads] = K . Q^T and O^T[D x 8] += V^T . P^T use
-//     mma.sync.m16n8k16 (bf16 in, fp32 accumulate) fed by ldmatrix(.trans) from
-//     the swizzled ring -- tensor cores here cut the instruction count (G = 8
-//     would need ~9 FMA-pipe ops per loaded element on SIMT), not the byte count.
-//     Online softmax per head in the log2 domain; row max by 3
-//     shuffles, the sum l is kept per lane and reduced once per item.  P is
-//     rounded to bf16 for the PV product (reading R12); l uses unrounded p.
+//   warp 0 (producer): walks the block table (one coalesced load per 32 sub-blocks,
+//     broadcast by shuffle) and for every 16-key sub-block of a paged block issues TMA
+//     tile loads (cp.async.bulk.tensor.4d, box {64 d, 1 head, 16 slots, 1 block},
+//     128B swizzle) of K and V into an NST-stage shared-memory ring guarded by
+//     mbarriers.  Sub-blocks wholly past the sequence end are never fetched.
+//   warps 1..NCW (consumers): sub-block g (CTA-global counter) goes to warp g % NCW.
+//     Scores S^T[16 keys x 8 heads] = K . Q^T and O^T[D x 8] += V^T . P^T use
+//     mma.sync.m16n8k16 (bf16 in, fp32 accumulate) fed by ldmatrix(.trans) from the
+//     swizzled ring -- tensor cores here cut the instruction count (G = 8 would need
+//     ~9 FMA-pipe ops per loaded element on SIMT), not the byte count.  Online softmax
+//     per head in the log2 domain; row max by 3 shuffles, the sum l is kept
+//     per lane and reduced once per item.  P is rounded to bf16 for the PV product
+//     (reading R12); l uses unrounded p.
 //   end of item: the NCW warp states are merged through shared memory; a
-//     single-segment sequence writes bf16 output directly (acc / l), otherwise
-//     the partial (m, l, acc) goes to the workspace for K3.
-// Slots at positions >= L_b of the last block may hold anything (NaN): scores are
+//     single-segment sequence writes bf16 output directly (acc / l), otherwise the
+//     partial (m, l, acc) goes to the workspace for K3.
+// Slots at positions >= L_b of the last sub-block may hold anything (NaN): scores are
 // masked by select and those V rows are zeroed in shared memory before use
 // (reading R13).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
 namespace pattn {
 namespace {
 
+constexpr int kSub = 16;  // keys per ring stage (one mma M tile)
+
 template <int D>
 struct DecodeShape {
   static constexpr int kHalves = D / 64;  // 128-byte (64 x bf16) swizzle atoms per row
   static constexpr int kKC = D / 16;      // k-chunks of the QK^T mma / m-tiles of the PV mma
+  static constexpr int kHalfBytes = kSub * 128;
+  static constexpr int kOpBytes = kHalves * kHalfBytes;  // K (or V) of one 16-key sub-block
+  static constexpr int kStageBytes = 2 * kOpBytes;
 };
 
 struct Item {
-  int b, c, kvh, hg, kb0, kb1, nseg, L, tok;
+  int b, c, kvh, hg, sb0, sb1, nseg, L, tok;
 };
 
+// Segment c of decode sequence b covers paged blocks [kb0, kb1) (K5's plan), i.e. 16-key
+// sub-blocks [kb0*bs/16, min(kb1*bs/16, ceil(L/16))).
 __device__ __forceinline__ Item decode_item(const Params& p, int it) {
   Item x;
   const int units = p.Hkv * p.HG;
@@ -57,8 +66,11 @@ __device__ __forceinline__ Item decode_item(const Params& p, int it) {
   x.tok = __ldg(p.cu_seqlens_q + x.b);
   const int nblk = (x.L + p.bs - 1) / p.bs;
   const int per = (nblk + x.nseg - 1) / x.nseg;
-  x.kb0 = (x.c - c0) * per;
-  x.kb1 = min(nblk, x.kb0 + per);
+  const int kb0 = (x.c - c0) * per;
+  const int kb1 = min(nblk, kb0 + per);
+  const int n16 = p.bs / kSub;
+  x.sb0 = kb0 * n16;
+  x.sb1 = min(kb1 * n16, (x.L + kSub - 1) / kSub);
   return x;
 }
 
@@ -69,12 +81,8 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
   using S = DecodeShape<D>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int bs = p.bs;
-  const int half_bytes = bs * 128;
-  const int op_bytes = S::kHalves * half_bytes;
-  const int stage_bytes = 2 * op_bytes;
   uint8_t* ring = smem;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)nst * stage_bytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)nst * S::kStageBytes);
   uint64_t* empty = full + nst;
   float* scratch = reinterpret_cast<float*>(empty + nst);  // [NCW][16 + 8*D]
   constexpr int kScr = 16 + 8 * D;
@@ -90,6 +98,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
   __syncthreads();
 
   const int n_items = p.hdr[kHdrTotalChunks] * p.Hkv * p.HG;
+  const int n16 = p.bs / kSub;
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
@@ -102,24 +111,25 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
     for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
       const Item x = decode_item(p, it);
       const int32_t* bt = p.block_table + (int64_t)x.b * p.bt_stride;
-      for (int j0 = x.kb0; j0 < x.kb1; j0 += 32) {
-        const int n = min(32, x.kb1 - j0);
-        const int id = lane < n ? __ldg(bt + j0 + lane) : 0;
+      for (int j0 = x.sb0; j0 < x.sb1; j0 += 32) {
+        const int n = min(32, x.sb1 - j0);
+        const int id = lane < n ? __ldg(bt + (j0 + lane) / n16) : 0;
         for (int jj = 0; jj < n; ++jj) {
           const int blk = __shfl_sync(0xffffffffu, id, jj);
+          const int slot0 = ((j0 + jj) % n16) * kSub;
           if (lane == 0) {
             const uint32_t s = g % nst;
             const uint32_t ph = (g / nst) & 1u;
-            mbar_wait(&empty[s], ph ^ 1u);
-            mbar_arrive_expect_tx(&full[s], stage_bytes);
-            uint8_t* st = ring + (size_t)s * stage_bytes;
-            const int c1 = p.kv_tok_inner ? 0 : x.kvh, c2 = p.kv_tok_inner ? x.kvh : 0;
+            mbar_wait_tag(&empty[s], ph ^ 1u, 1000000 + (int)g, it, 0);
+            mbar_arrive_expect_tx(&full[s], S::kStageBytes);
+            uint8_t* st = ring + (size_t)s * S::kStageBytes;
+            const int c1 = p.kv_tok_inner ? slot0 : x.kvh, c2 = p.kv_tok_inner ? x.kvh : slot0;
 #pragma unroll
             for (int h = 0; h < S::kHalves; ++h)
-              tma_load_4d_hint(st + h * half_bytes, &tmK, &full[s], h * 64, c1, c2, blk, policy);
+              tma_load_4d_hint(st + h * S::kHalfBytes, &tmK, &full[s], h * 64, c1, c2, blk, policy);
 #pragma unroll
             for (int h = 0; h < S::kHalves; ++h)
-              tma_load_4d_hint(st + op_bytes + h * half_bytes, &tmV, &full[s], h * 64, c1, c2, blk, policy);
+              tma_load_4d_hint(st + S::kOpBytes + h * S::kHalfBytes, &tmV, &full[s], h * 64, c1, c2, blk, policy);
           }
           ++g;
         }
@@ -130,9 +140,8 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
 
   // -------------------------------------------------------------- consumers
   const int cw = warp - 1;
-  const int r = lane >> 2, c = lane & 3;   // mma fragment coordinates
+  const int r = lane >> 2, c = lane & 3;       // mma fragment coordinates
   const int mat = lane >> 3, mrow = lane & 7;  // ldmatrix source coordinates
-  const int nsub = bs >> 4;
   float* scr = scratch + cw * kScr;
   __nv_bfloat16* O = static_cast<__nv_bfloat16*>(p.out);
   const __nv_bfloat16* Q = static_cast<const __nv_bfloat16*>(p.q);
@@ -160,89 +169,85 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
 #pragma unroll
     for (int t = 0; t < S::kKC; ++t) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0.f;
 
-    const int nblk_item = x.kb1 - x.kb0;
-    for (int j = cw; j < nblk_item; j += NCW) {
+    const int nsb = x.sb1 - x.sb0;
+    // Sub-block g (CTA-global counter) goes to consumer warp g % NCW, and nst is a multiple
+    // of NCW, so every ring stage is always consumed by the same warp, in order.  (TMA loads
+    // complete out of order: a waiter must have observed phase u-1 of a stage before it
+    // waits on phase u, otherwise the parity test aliases and returns early.)
+    const int j_first = (int)((cw + NCW - (g % NCW)) % NCW);
+    for (int j = j_first; j < nsb; j += NCW) {
       const uint32_t gg = g + j;
       const uint32_t s = gg % nst;
-      mbar_wait(&full[s], (gg / nst) & 1u);
-      const uint32_t kst = ring_u32 + s * stage_bytes;
-      const uint32_t vst = kst + op_bytes;
-      const int kpos0 = (x.kb0 + j) * bs;
-      const int valid = x.L - kpos0;  // slots [0, valid) hold real keys
-      if (valid < bs) {
+      mbar_wait_tag(&full[s], (gg / nst) & 1u, (int)gg, it, j);
+      const uint32_t kst = ring_u32 + s * S::kStageBytes;
+      const uint32_t vst = kst + S::kOpBytes;
+      const int valid = x.L - (x.sb0 + j) * kSub;  // slots [0, valid) hold real keys
+      if (valid < kSub) {
         // zero V rows past the sequence end (they may hold NaN; 0 * NaN = NaN in the mma)
-        uint8_t* vgen = ring + (size_t)s * stage_bytes + op_bytes;
-        const int nrow = bs - valid;
+        uint8_t* vgen = ring + (size_t)s * S::kStageBytes + S::kOpBytes;
+        const int nrow = kSub - valid;
         for (int e = lane; e < nrow * 8 * S::kHalves; e += 32) {
           const int h = e / (nrow * 8);
           const int rem = e - h * nrow * 8;
           const int row = valid + rem / 8;
           const int ch = rem & 7;
-          *reinterpret_cast<uint4*>(vgen + h * half_bytes + row * 128 + ch * 16) = make_uint4(0, 0, 0, 0);
+          *reinterpret_cast<uint4*>(vgen + h * S::kHalfBytes + row * 128 + ch * 16) = make_uint4(0, 0, 0, 0);
         }
         __syncwarp();
       }
-      for (int sub = 0; sub < nsub; ++sub) {
-        float sc[4] = {0.f, 0.f, 0.f, 0.f};
+      float sc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-        for (int kc = 0; kc < S::kKC; ++kc) {
-          const int key = sub * 16 + (mat & 1) * 8 + mrow;
-          const int dd = kc * 16 + (mat >> 1) * 8;
-          const uint32_t addr =
-              kst + (dd >> 6) * half_bytes + key * 128 + ((((dd & 63) >> 3) ^ (key & 7)) << 4);
-          uint32_t a0, a1, a2, a3;
-          ldmatrix_x4(addr, a0, a1, a2, a3);
-          mma_bf16_16816(sc, a0, a1, a2, a3, bq[kc][0], bq[kc][1]);
-        }
-        // sc[0..1]: key (sub*16 + r), heads 2c, 2c+1; sc[2..3]: key + 8
-        const int key0 = sub * 16 + r;
-        const float s0 = key0 < valid ? sc[0] * p.scale_log2 : -INFINITY;
-        const float s1 = key0 < valid ? sc[1] * p.scale_log2 : -INFINITY;
-        const float s2 = key0 + 8 < valid ? sc[2] * p.scale_log2 : -INFINITY;
-        const float s3 = key0 + 8 < valid ? sc[3] * p.scale_log2 : -INFINITY;
-        float mt0 = fmaxf(s0, s2), mt1 = fmaxf(s1, s3);
+      for (int kc = 0; kc < S::kKC; ++kc) {
+        const int key = (mat & 1) * 8 + mrow;
+        const int dd = kc * 16 + (mat >> 1) * 8;
+        const uint32_t addr = kst + (dd >> 6) * S::kHalfBytes + key * 128 + ((((dd & 63) >> 3) ^ (key & 7)) << 4);
+        uint32_t a0, a1, a2, a3;
+        ldmatrix_x4(addr, a0, a1, a2, a3);
+        mma_bf16_16816(sc, a0, a1, a2, a3, bq[kc][0], bq[kc][1]);
+      }
+      // sc[0..1]: key r, heads 2c, 2c+1; sc[2..3]: key r + 8
+      const float s0 = r < valid ? sc[0] * p.scale_log2 : -INFINITY;
+      const float s1 = r < valid ? sc[1] * p.scale_log2 : -INFINITY;
+      const float s2 = r + 8 < valid ? sc[2] * p.scale_log2 : -INFINITY;
+      const float s3 = r + 8 < valid ? sc[3] * p.scale_log2 : -INFINITY;
+      float mt0 = fmaxf(s0, s2), mt1 = fmaxf(s1, s3);
 #pragma unroll
-        for (int o = 4; o < 32; o <<= 1) {
-          mt0 = fmaxf(mt0, __shfl_xor_sync(0xffffffffu, mt0, o));
-          mt1 = fmaxf(mt1, __shfl_xor_sync(0xffffffffu, mt1, o));
-        }
-        const float mn0 = fmaxf(m0, mt0), mn1 = fmaxf(m1, mt1);
-        // sub-tile with no valid key at all (only possible for sub > 0 of a last block)
-        const float base0 = mn0 == -INFINITY ? 0.f : mn0;
-        const float base1 = mn1 == -INFINITY ? 0.f : mn1;
-        const float al0 = fast_exp2(m0 - base0), al1 = fast_exp2(m1 - base1);
-        const float p0 = fast_exp2(s0 - base0), p1 = fast_exp2(s1 - base1);
-        const float p2 = fast_exp2(s2 - base0), p3 = fast_exp2(s3 - base1);
-        l0 = fmaf(l0, al0, p0 + p2);
-        l1 = fmaf(l1, al1, p1 + p3);
-        m0 = mn0;
-        m1 = mn1;
+      for (int o = 4; o < 32; o <<= 1) {
+        mt0 = fmaxf(mt0, __shfl_xor_sync(0xffffffffu, mt0, o));
+        mt1 = fmaxf(mt1, __shfl_xor_sync(0xffffffffu, mt1, o));
+      }
+      const float mn0 = fmaxf(m0, mt0), mn1 = fmaxf(m1, mt1);  // finite: every sub-block has a valid key
+      const float al0 = fast_exp2(m0 - mn0), al1 = fast_exp2(m1 - mn1);
+      const float p0 = fast_exp2(s0 - mn0), p1 = fast_exp2(s1 - mn1);
+      const float p2 = fast_exp2(s2 - mn0), p3 = fast_exp2(s3 - mn1);
+      l0 = fmaf(l0, al0, p0 + p2);
+      l1 = fmaf(l1, al1, p1 + p3);
+      m0 = mn0;
+      m1 = mn1;
 #pragma unroll
-        for (int t = 0; t < S::kKC; ++t) {
-          acc[t][0] *= al0;
-          acc[t][1] *= al1;
-          acc[t][2] *= al0;
-          acc[t][3] *= al1;
-        }
-        // P^T as the B operand of O^T = V^T . P^T (transpose the 8x8 halves in registers)
-        const uint32_t pb0 = movmatrix_trans(pack_bf16(p0, p1));
-        const uint32_t pb1 = movmatrix_trans(pack_bf16(p2, p3));
+      for (int t = 0; t < S::kKC; ++t) {
+        acc[t][0] *= al0;
+        acc[t][1] *= al1;
+        acc[t][2] *= al0;
+        acc[t][3] *= al1;
+      }
+      // P^T as the B operand of O^T = V^T . P^T (transpose the 8x8 halves in registers)
+      const uint32_t pb0 = movmatrix_trans(pack_bf16(p0, p1));
+      const uint32_t pb1 = movmatrix_trans(pack_bf16(p2, p3));
 #pragma unroll
-        for (int t = 0; t < S::kKC; ++t) {
-          const int key = sub * 16 + (mat >> 1) * 8 + mrow;
-          const int dd = t * 16 + (mat & 1) * 8;
-          const uint32_t addr =
-              vst + (dd >> 6) * half_bytes + key * 128 + ((((dd & 63) >> 3) ^ (key & 7)) << 4);
-          uint32_t a0, a1, a2, a3;
-          ldmatrix_x4_trans(addr, a0, a1, a2, a3);
-          mma_bf16_16816(acc[t], a0, a1, a2, a3, pb0, pb1);
-        }
+      for (int t = 0; t < S::kKC; ++t) {
+        const int key = (mat >> 1) * 8 + mrow;
+        const int dd = t * 16 + (mat & 1) * 8;
+        const uint32_t addr = vst + (dd >> 6) * S::kHalfBytes + key * 128 + ((((dd & 63) >> 3) ^ (key & 7)) << 4);
+        uint32_t a0, a1, a2, a3;
+        ldmatrix_x4_trans(addr, a0, a1, a2, a3);
+        mma_bf16_16816(acc[t], a0, a1, a2, a3, pb0, pb1);
       }
       __syncwarp();
-      if (valid < bs) fence_proxy_async_smem();  // generic zero-writes before the next TMA fill
+      if (valid < kSub) fence_proxy_async_smem();  // generic zero-writes before the next TMA fill
       if (lane == 0) mbar_arrive(&empty[s]);
     }
-    g += nblk_item;
+    g += nsb;
 
     // ---- merge the NCW warp states of this item
 #pragma unroll
@@ -293,36 +298,55 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
   }
 }
 
-constexpr int kNCW = 4;
+template <int D, int NCW>
+cudaError_t launch_dw(const Params& p, const DecodeLaunch& dl, const CUtensorMap& tmK, const CUtensorMap& tmV,
+                      cudaStream_t stream) {
+  auto kern = k2_decode<D, NCW>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dl.smem);
+  if (e != cudaSuccess) return e;
+  kern<<<dl.grid, (NCW + 1) * 32, dl.smem, stream>>>(tmK, tmV, p, dl.stages);
+  return cudaGetLastError();
+}
 
 template <int D>
 cudaError_t launch_d(const Params& p, const DecodeLaunch& dl, const CUtensorMap& tmK, const CUtensorMap& tmV,
                      cudaStream_t stream) {
-  auto kern = k2_decode<D, kNCW>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dl.smem);
-  if (e != cudaSuccess) return e;
-  kern<<<dl.grid, (kNCW + 1) * 32, dl.smem, stream>>>(tmK, tmV, p, dl.stages);
-  return cudaGetLastError();
+  if (dl.consumer_warps == 8) return launch_dw<D, 8>(p, dl, tmK, tmV, stream);
+  return launch_dw<D, 4>(p, dl, tmK, tmV, stream);
+}
+
+int env_or(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return (v && *v) ? atoi(v) : dflt;
 }
 
 }  // namespace
 
+// Launch shape: one or two CTAs per SM, each with 1 producer + NCW consumer warps and an
+// NST-stage ring; ~160 KB of K/V in flight per SM.  Env overrides for sweeps:
+// PATTN_DECODE_WARPS (4|8), PATTN_DECODE_CTAS (1|2), PATTN_DECODE_RING_KB.
 DecodeLaunch plan_decode(const Params& p, int num_sms, size_t max_smem) {
   DecodeLaunch dl;
-  dl.consumer_warps = kNCW;
-  const size_t stage = (size_t)4 * p.bs * p.D;  // K + V of one block, bf16
-  const size_t scratch = (size_t)kNCW * (16 + 8 * p.D) * sizeof(float);
+  dl.consumer_warps = env_or("PATTN_DECODE_WARPS", 4) == 8 ? 8 : 4;
+  int ctas = env_or("PATTN_DECODE_CTAS", 3);
+  if (ctas < 1) ctas = 1;
+  if (ctas > 4) ctas = 4;
+  const size_t stage = (size_t)4 * kSub * p.D;  // K + V of one 16-key sub-block, bf16
+  const size_t scratch = (size_t)dl.consumer_warps * (16 + 8 * p.D) * sizeof(float);
   const size_t fixed = 1024 /*align slack*/ + scratch;
-  const size_t budget = max_smem > fixed ? max_smem - fixed : 0;
-  size_t want = 160 * 1024;
+  const size_t per_cta = (max_smem < 228 * 1024 ? max_smem : 228 * 1024) / ctas - 1024;
+  const size_t budget = per_cta > fixed ? per_cta - fixed : 0;
+  size_t want = (size_t)env_or("PATTN_DECODE_RING_KB", 64) * 1024;
   if (want > budget) want = budget;
   int st = (int)(want / (stage + 16));
-  if (st > 32) st = 32;
-  if (st < 2) st = 2;
+  if (st > 64) st = 64;
+  st -= st % dl.consumer_warps;  // stage s is always consumed by warp s % NCW (see kernel)
+  if (st < dl.consumer_warps) st = dl.consumer_warps;
   dl.stages = st;
   dl.smem = fixed + (size_t)st * (stage + 16);
   const long long max_items = (long long)p.max_chunks * p.Hkv * p.HG;
-  dl.grid = (int)(max_items < num_sms ? max_items : num_sms);
+  const long long g = (long long)num_sms * ctas;
+  dl.grid = (int)(max_items < g ? max_items : g);
   if (dl.grid < 1) dl.grid = 1;
   return dl;
 }

@@ -63,6 +63,13 @@ int env_int(const char* name, int dflt) {
   return (v && *v) ? atoi(v) : dflt;
 }
 
+thread_local char g_last_error[256] = "";
+
+pattn_status_t cuda_fail(cudaError_t e) {
+  snprintf(g_last_error, sizeof(g_last_error), "%s: %s", cudaGetErrorName(e), cudaGetErrorString(e));
+  return PATTN_ERR_CUDA;
+}
+
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 bool aligned16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15u) == 0; }
 
@@ -147,7 +154,7 @@ pattn_status_t make_plan(const pattn_problem_t* p, const void* q, const void* kc
                       (kc == nullptr || aligned16(kc)) && (vc == nullptr || aligned16(vc));
   const bool q_ok = (p->q_stride_tok % 8 == 0) && (p->q_stride_head % 8 == 0) && (q == nullptr || aligned16(q));
   const bool o_ok = (p->o_stride_tok % 8 == 0) && (p->o_stride_head % 8 == 0) && (out == nullptr || aligned16(out));
-  pl->use_k2 = bf16 && !generic && p->block_size % 16 == 0 && p->block_size <= 256 && tma_ok && q_ok && o_ok;
+  pl->use_k2 = bf16 && !generic && p->block_size % 16 == 0 && tma_ok && q_ok && o_ok;
 
   Params probe;
   fill_params(p, *pl, &probe);
@@ -226,7 +233,7 @@ bool encode_kv_map(CUtensorMap* tm, const pattn_problem_t* p, const void* base, 
     dims[2] = (cuuint64_t)p->num_kv_heads;
     strides[0] = (cuuint64_t)p->kv_stride_tok * 2;
     strides[1] = (cuuint64_t)p->kv_stride_head * 2;
-    box[1] = (cuuint32_t)p->block_size;
+    box[1] = 16;  // one 16-key sub-block of a paged block
     box[2] = 1;
   } else {
     dims[1] = (cuuint64_t)p->num_kv_heads;
@@ -234,7 +241,7 @@ bool encode_kv_map(CUtensorMap* tm, const pattn_problem_t* p, const void* base, 
     strides[0] = (cuuint64_t)p->kv_stride_head * 2;
     strides[1] = (cuuint64_t)p->kv_stride_tok * 2;
     box[1] = 1;
-    box[2] = (cuuint32_t)p->block_size;
+    box[2] = 16;  // one 16-key sub-block of a paged block
   }
   dims[3] = (cuuint64_t)p->num_blocks;
   strides[2] = (cuuint64_t)p->kv_stride_blk * 2;
@@ -322,7 +329,7 @@ pattn_status_t run(const pattn_problem_t* p, const void* q, const void* k_cache,
   ev.rec(2 * PATTN_KERNEL_METADATA, s1);
   e = launch_metadata(k, s1);
   ev.rec(2 * PATTN_KERNEL_METADATA + 1, s1);
-  if (e != cudaSuccess) return PATTN_ERR_CUDA;
+  if (e != cudaSuccess) return cuda_fail(e);
   if (metadata_only) return PATTN_OK;
 
   cudaEvent_t fork = nullptr, join = nullptr;
@@ -338,23 +345,23 @@ pattn_status_t run(const pattn_problem_t* p, const void* q, const void* k_cache,
     ev.rec(2 * PATTN_KERNEL_DECODE, sd);
     e = launch_decode(k, pl.dl, tmK, tmV, sd);
     ev.rec(2 * PATTN_KERNEL_DECODE + 1, sd);
-    if (e != cudaSuccess) return PATTN_ERR_CUDA;
+    if (e != cudaSuccess) return cuda_fail(e);
     ev.rec(2 * PATTN_KERNEL_REDUCE, sd);
     e = launch_reduce(k, sd);
     ev.rec(2 * PATTN_KERNEL_REDUCE + 1, sd);
-    if (e != cudaSuccess) return PATTN_ERR_CUDA;
+    if (e != cudaSuccess) return cuda_fail(e);
   }
   if (pl.use_k1) {
     ev.rec(2 * PATTN_KERNEL_PREFILL, s1);
     e = launch_prefill(k, pl.pl, tmQ, tmK, tmV, s1);
     ev.rec(2 * PATTN_KERNEL_PREFILL + 1, s1);
-    if (e != cudaSuccess) return PATTN_ERR_CUDA;
+    if (e != cudaSuccess) return cuda_fail(e);
   }
   if (pl.use_k4) {
     ev.rec(2 * PATTN_KERNEL_GENERIC, s1);
     e = launch_generic(k, pl.k4_grid, pl.rpw, s1);
     ev.rec(2 * PATTN_KERNEL_GENERIC + 1, s1);
-    if (e != cudaSuccess) return PATTN_ERR_CUDA;
+    if (e != cudaSuccess) return cuda_fail(e);
   }
   if (two) {
     cudaEventRecord(join, s2);
@@ -519,6 +526,16 @@ int32_t pattn_planned_launches(const pattn_problem_t* p) {
   return 1 + (pl.use_k1 ? 1 : 0) + (pl.use_k4 ? 1 : 0) + (pl.use_k2 ? 2 : 0);
 }
 
+int32_t pattn_planned_kernels(const pattn_problem_t* p) {
+  Plan pl;
+  if (make_plan(p, nullptr, nullptr, nullptr, nullptr, &pl) != PATTN_OK) return 0;
+  return (1 << PATTN_KERNEL_METADATA) | (pl.use_k1 ? 1 << PATTN_KERNEL_PREFILL : 0) |
+         (pl.use_k2 ? (1 << PATTN_KERNEL_DECODE) | (1 << PATTN_KERNEL_REDUCE) : 0) |
+         (pl.use_k4 ? 1 << PATTN_KERNEL_GENERIC : 0);
+}
+
 int32_t pattn_version(void) { return kVersion; }
+
+const char* pattn_last_error(void) { return g_last_error; }
 
 }  // extern "C"

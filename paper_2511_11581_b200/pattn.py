@@ -85,6 +85,8 @@ EXPORTS = [
     "pattn_validate_metadata_host",
     "pattn_debug_plan",
     "pattn_planned_launches",
+    "pattn_planned_kernels",
+    "pattn_last_error",
     "pattn_version",
 ]
 
@@ -118,14 +120,18 @@ def load() -> ctypes.CDLL:
             lib.pattn_debug_plan.argtypes = [P, vp, vp, vp, ctypes.c_int32, vp, sz, vp]
             lib.pattn_planned_launches.restype = ctypes.c_int32
             lib.pattn_planned_launches.argtypes = [P]
+            lib.pattn_planned_kernels.restype = ctypes.c_int32
+            lib.pattn_planned_kernels.argtypes = [P]
             lib.pattn_version.restype = ctypes.c_int32
+            lib.pattn_last_error.restype = ctypes.c_char_p
             _lib = lib
     return _lib
 
 
 def _check(code: int, where: str):
     if code != PATTN_OK:
-        raise PattnError(code, where)
+        detail = load().pattn_last_error().decode() if code == 7 else ""
+        raise PattnError(code, f"{where} {detail}".strip())
 
 
 def _dtype_code(t: torch.Tensor) -> int:
@@ -334,6 +340,23 @@ def validate_metadata_host(problem: Problem, cu_seqlens_q, seq_lens, block_table
 
 def planned_launches(problem: Problem) -> int:
     return int(load().pattn_planned_launches(ctypes.byref(problem)))
+
+
+def planned_kernels(problem: Problem) -> int:
+    """Bit mask of kernel kinds (1 << KERNEL_*) the call launches."""
+    return int(load().pattn_planned_kernels(ctypes.byref(problem)))
+
+
+def make_events(n_steps: int):
+    """Per-step lists of 2*KERNEL_COUNT timing events for the `events=` option.  Each event is
+    recorded once here so torch materialises it; the library re-records it around its kernel."""
+    out = []
+    for _ in range(n_steps):
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(2 * KERNEL_COUNT)]
+        for e in evs:
+            e.record()
+        out.append(evs)
+    return out
 
 
 def version() -> int:

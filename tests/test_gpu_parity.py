@@ -85,6 +85,25 @@ def test_long_decode_split(flags):
     _check(batch, flags, f"long decode flags={flags}")
 
 
+PREFILL_CASES = [
+    # (seqs, heads, bs, layout)
+    (((0, 1000), (2000, 300), (0, 129), (77, 1)), (32, 8), 16, "NHD"),
+    (((0, 777), (130, 260)), (64, 8), 16, "NHD"),
+    (((0, 515), (1000, 64)), (32, 8), 64, "HND"),
+    (((3, 200), (0, 47)), (16, 1), 32, "NHD"),
+    (((0, 300),), (8, 8), 16, "NHD"),       # G = 1: BLOCK_Q = 128
+    (((0, 257), (9, 9)), (128, 2), 128, "NHD"),  # G = 64: BLOCK_Q = 2; bs 128 = one block per tile
+]
+
+
+@pytest.mark.parametrize("case", range(len(PREFILL_CASES)))
+def test_prefill_tensor_core_path(case):
+    seqs, heads, bs, layout = PREFILL_CASES[case]
+    w = Workload(f"prefill{case}", seqs, heads[0], heads[1], 128, bs, "bf16")
+    batch = generate(w, seed=100 + case, dist="peaked", layout=layout)
+    _check(batch, 0, f"prefill case {case}")
+
+
 def test_chunked_prefill_and_empty_sequences():
     w = Workload("chunked", ((300, 40), (0, 0), (77, 1), (5, 129), (0, 0), (0, 33)), 32, 8, 128, 16, "bf16")
     batch = generate(w, seed=6, dist="peaked")

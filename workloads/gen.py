@@ -272,6 +272,55 @@ def generate(
     )
 
 
+def generate_device(w: Workload, seed: int, device="cuda", layout: str = "NHD", spare_blocks: int = 8):
+    """Same structure as generate() (U[-1,1] values rounded to the dtype, permuted physical
+    blocks, -1 padded block table) drawn with torch's generator directly on the device, for
+    the large bench workloads.  Unused cache slots hold finite values (timing runs).
+    Returns a dict of device tensors plus host copies of the metadata."""
+    import torch
+
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    B, Hq, Hkv, D, bs = w.num_seqs, w.num_q_heads, w.num_kv_heads, w.head_dim, w.block_size
+    q_lens = torch.tensor([q for _, q in w.seqs], dtype=torch.int64)
+    seq_lens = torch.tensor([c + q for c, q in w.seqs], dtype=torch.int64)
+    nblk = (seq_lens + bs - 1) // bs
+    num_blocks = int(nblk.sum()) + spare_blocks
+    max_blocks = max(1, int(nblk.max()))
+    T = int(q_lens.sum())
+    tdt = torch.bfloat16 if w.dtype == "bf16" else torch.float32
+
+    def uni(shape):
+        out = torch.empty(shape, dtype=tdt, device=device)
+        flat = out.view(-1)
+        chunk = 1 << 27
+        for s in range(0, flat.numel(), chunk):
+            e = min(flat.numel(), s + chunk)
+            x = torch.rand(e - s, generator=g, device=device, dtype=torch.float32)
+            flat[s:e] = (x * 2.0 - 1.0).to(tdt)
+        return out
+
+    kv_shape = (num_blocks, bs, Hkv, D) if layout == "NHD" else (num_blocks, Hkv, bs, D)
+    q = uni((T, Hq, D))
+    k = uni(kv_shape)
+    v = uni(kv_shape)
+    perm = torch.randperm(num_blocks, generator=g, device=device).to(torch.int32).cpu()
+    bt = torch.full((B, max_blocks), -1, dtype=torch.int32)
+    off = 0
+    for b in range(B):
+        n = int(nblk[b])
+        bt[b, :n] = perm[off : off + n]
+        off += n
+    cu = torch.zeros(B + 1, dtype=torch.int32)
+    cu[1:] = torch.cumsum(q_lens, 0).to(torch.int32)
+    return dict(
+        q=q, k_cache=k, v_cache=v,
+        block_table=bt.to(device), cu_seqlens_q=cu.to(device), seq_lens=seq_lens.to(torch.int32).to(device),
+        block_table_h=bt, cu_seqlens_q_h=cu, seq_lens_h=seq_lens.to(torch.int32),
+        layout=layout, num_blocks=num_blocks,
+    )
+
+
 def random_workload(
     rng: np.random.Generator,
     heads: Tuple[int, int],
