@@ -2,59 +2,69 @@
 //
 // PAPER.md §4.4 "Prefill and GQA Optimization" (App. B): a Q block packs
 // BLOCK_Q consecutive query tokens x the G query heads that share one KV head into a
-// BLOCK_M = 128-row tile (token-major / head-minor, reading R8), so every K/V tile is
-// loaded once per Q block and shared by all 128 rows.  KV tiles of 128 keys span
-// 128/bs paged blocks (tile size decoupled from BLOCK_SIZE, §4.6); the tiled
-// (online) softmax of §4.1 runs between the two contractions.
+// BLOCK_M-row tile (token-major / head-minor, reading R8), so every K/V tile is loaded once
+// per Q block and shared by all rows.  Here BLOCK_M = 256 = two 128-row halves (a, b), each
+// its own UMMA M=128 accumulator, so BLOCK_Q = 256/G.  KV tiles of 128 keys = 8 sub-blocks
+// of 16 keys gathered through the block table from any block size that is a multiple of 16
+// (tile size decoupled from BLOCK_SIZE, §4.6).  The tiled (online) softmax of
+// §4.1 runs between the two contractions.
 //
 // One CTA per SM, persistent over (Q block, KV head) work items (static launch grid,
-// P:401-406), longest (last) Q blocks first.  Warp roles (256 threads):
-//   warp 0      TMA producer: Q tile (4-D map over q viewed [T][Hkv][G][D], 2 boxes),
-//               K and V tiles (one 4-D box per paged block and 64-wide d half, through
-//               the block table; blocks past the visible range are requested out of
-//               bounds so TMA zero-fills them) into 2-stage K and V rings.
-//   warp 1      MMA issuer (one thread): S = Q K^T (M=128, N=128, K=16 x 8) into a
-//               double-buffered TMEM S tile; O += P V (P from shared memory, V MN-major)
-//               into the TMEM O accumulator; tcgen05.commit -> mbarriers.
-//   warp 2      TMEM allocator (512 columns: O | S0 | S1).
-//   warps 4..7  softmax / correction / epilogue: thread r owns row r (TMEM lane r):
-//               tcgen05.ld of the S row, causal mask (row limit ctx+i+1),
-//               max, exp2, row sum; lazy rescale of O in TMEM only when the running
-//               max grows by > 2^8 (exact: p <= 256 otherwise); P (bf16) written to
-//               shared memory in the UMMA K-major SW128 layout; epilogue O / l -> bf16.
-// V rows past the sequence end inside the last paged block may hold NaN (reading R13):
-// the softmax warps zero them in shared memory before the PV product.
+// P:401-406), longest (last) Q blocks first.  Warp roles (384 threads):
+//   warp 0       TMA producer: Q (both halves, 4 boxes) and the K / V tiles (2 boxes per
+//                16-key sub-block; sub-blocks past the visible range are requested at block
+//                index num_blocks, out of bounds, so TMA zero-fills them) into K and V rings.
+//   warp 1       MMA issuer (one thread), per KV tile j:
+//                  PV_a(j-1)  O_a += P_a V   (P_a bf16 in TMEM, aliased on S_a; V MN-major smem)
+//                  S_a(j)     S_a  = Q_a K^T (Q, K K-major SW128 smem)
+//                  PV_b(j-1), S_b(j)
+//                so the two softmax warpgroups ping-pong: while one works on its S tile the
+//                tensor pipe runs the other half's PV and S.  tcgen05.commit -> mbarriers.
+//   warp 2       TMEM allocator: 512 columns = S_a | S_b | O_a | O_b (128 each).
+//   warps 4..7   softmax WG a (thread r owns row r of half a = TMEM lane r)
+//   warps 8..11  softmax WG b: tcgen05.ld of the S row, causal mask (row limit ctx+i+1,
+//                P:316-317), max, exp2, row sum; lazy rescale of O in TMEM only when the
+//                running max grows by > 2^8 (exact: p <= 256 otherwise); P (bf16) written
+//                back into TMEM over S with tcgen05.st; epilogue O / l -> bf16 -> out.
+// V rows past the sequence end inside the last sub-block may hold NaN (reading R13): WG a
+// zeroes them in shared memory before PV_a (PV_b is issued after PV_a).
 #include "common.cuh"
 #include "kernels.h"
 
 namespace pattn {
 namespace {
 
-constexpr int kM = 128;        // BLOCK_M rows per Q tile
+constexpr int kHalfM = 128;    // rows per half (one UMMA M)
+constexpr int kM = 2 * kHalfM; // BLOCK_M
 constexpr int kN = 128;        // keys per KV tile
 constexpr int kD = 128;        // head dim
-constexpr int kThreads = 256;  // 8 warps
-constexpr uint32_t kTile = kN * kD * 2;     // 32 KB: one bf16 128x128 tile
-constexpr uint32_t kHalf = kTile / 2;       // 16 KB: one 64-wide d (or key) half
-constexpr int kStages = 2;
-constexpr float kRescaleThreshold = 8.0f;  // log2 domain: rescale O only if max grows by > 2^8
+constexpr int kThreads = 384;  // 12 warps
+constexpr uint32_t kTile = kN * kD * 2;  // 32 KB: one bf16 128x128 tile
+constexpr uint32_t kHalf = kTile / 2;    // 16 KB: one 64-wide d half
+constexpr int kKStages = 3;
+constexpr int kVStages = 2;
+constexpr float kRescaleThreshold = 8.0f;  // log2 domain: rescale O only if the max grows by > 2^8
 
 // shared-memory map (offsets from a 1024-aligned base)
-constexpr uint32_t kOffQ = 0;
-constexpr uint32_t kOffP = kOffQ + kTile;
-constexpr uint32_t kOffK = kOffP + kTile;
-constexpr uint32_t kOffV = kOffK + kStages * kTile;
-constexpr uint32_t kOffBar = kOffV + kStages * kTile;
+constexpr uint32_t kOffQ = 0;  // half a: [0, 32K), half b: [32K, 64K)
+constexpr uint32_t kOffK = kOffQ + 2 * kTile;
+constexpr uint32_t kOffV = kOffK + kKStages * kTile;
+constexpr uint32_t kOffBar = kOffV + kVStages * kTile;
 constexpr uint32_t kSmemBytes = kOffBar + 256 + 1024;
+static_assert(kSmemBytes <= 227 * 1024, "shared memory budget");
+
+// TMEM columns
+constexpr uint32_t kTmemS = 0;    // S_x at x*128 (P_x aliased on its first 64 columns)
+constexpr uint32_t kTmemO = 256;  // O_x at 256 + x*128
 
 struct Bars {
   uint64_t q_full, q_empty;
-  uint64_t k_full[kStages], k_empty[kStages];
-  uint64_t v_full[kStages], v_empty[kStages];
-  uint64_t s_full[2], s_empty[2];
-  uint64_t p_full, pv_done, o_empty;
+  uint64_t k_full[kKStages], k_empty[kKStages];
+  uint64_t v_full[kVStages], v_empty[kVStages];
+  uint64_t s_full[2], p_full[2], pv_done[2], o_empty[2];
   uint32_t tmem_base;
 };
+static_assert(sizeof(Bars) <= 256, "barrier block");
 
 struct Item {
   int b, kvh, q0, qlen, L, ctx, tok0, ntok, kv_end, ntiles;
@@ -77,6 +87,16 @@ __device__ __forceinline__ Item prefill_item(const Params& p, int total_qb, int 
   return x;
 }
 
+// O[tmem] (+)= A[tmem] * B[smem desc]; kind::f16, A (P) K-major in TMEM.
+PATTN_DEVICE void tc_mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accum)
+      : "memory");
+}
+
 __global__ void __launch_bounds__(kThreads, 1)
     k1_prefill(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                const __grid_constant__ CUtensorMap tmV, Params p) {
@@ -89,19 +109,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     mbar_init(&bar.q_full, 1);
     mbar_init(&bar.q_empty, 1);
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < kKStages; ++s) {
       mbar_init(&bar.k_full[s], 1);
       mbar_init(&bar.k_empty[s], 1);
+    }
+    for (int s = 0; s < kVStages; ++s) {
       mbar_init(&bar.v_full[s], 1);
       mbar_init(&bar.v_empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&bar.s_full[b], 1);
-      mbar_init(&bar.s_empty[b], kM);
+    for (int h = 0; h < 2; ++h) {
+      mbar_init(&bar.s_full[h], 1);
+      mbar_init(&bar.p_full[h], kHalfM);
+      mbar_init(&bar.pv_done[h], 1);
+      mbar_init(&bar.o_empty[h], kHalfM);
     }
-    mbar_init(&bar.p_full, kM);
-    mbar_init(&bar.pv_done, 1);
-    mbar_init(&bar.o_empty, kM);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc(&bar.tmem_base, 512);
@@ -109,22 +130,25 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = bar.tmem_base;
-  const uint32_t tmem_O = tmem;                   // columns [0, 128)
-  const uint32_t tmem_S0 = tmem + 128;            // S buffer b at 128 + 128*b
 
   const int total_qb = p.hdr[kHdrTotalQBlocks];
   const int n_items = total_qb * p.Hkv;
   const int G = p.G;
+  const int bq_half = p.block_q / 2;  // tokens per 128-row half
+
+  // register rebalancing per warpgroup: producer/MMA warpgroup 56, softmax warpgroups 224
+  // (128*56 + 256*224 = 64512 <= 65536)
 
   if (warp == 0) {
     // ================================================================ TMA producer
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
     if (lane == 0) {
       tma_prefetch_desc(&tmQ);
       tma_prefetch_desc(&tmK);
       tma_prefetch_desc(&tmV);
     }
-    // A 128-key tile = 8 sub-blocks of 16 keys; sub-block i of tile jt is slots
-    // [(idx % n16)*16, +16) of paged block bt[idx / n16], idx = 8*jt + i (any bs = 16k).
+    // A 128-key tile = 8 sub-blocks of 16 keys; sub-block idx is slots [(idx % n16)*16, +16)
+    // of paged block bt[idx / n16] (any block size that is a multiple of 16).
     constexpr int nbt = kN / 16;
     const int n16 = p.bs / 16;
     const uint64_t pol_kv = l2_policy_evict_last();  // K/V tiles are re-read by the sequence's other Q blocks
@@ -134,222 +158,233 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int32_t* bt = p.block_table + (int64_t)x.b * p.bt_stride;
       const int nsb_valid = (x.kv_end + 15) / 16;  // sub-blocks holding visible keys
       if (lane == 0) {
-        mbar_wait_tag(&bar.q_empty, (ic & 1u) ^ 1u, 1,(int)ic,it);
-        mbar_arrive_expect_tx(&bar.q_full, kTile);
-        tma_load_4d(smem + kOffQ, &tmQ, &bar.q_full, 0, 0, x.kvh, x.q0 + x.tok0);
-        tma_load_4d(smem + kOffQ + kHalf, &tmQ, &bar.q_full, 64, 0, x.kvh, x.q0 + x.tok0);
+        mbar_wait(&bar.q_empty, (ic & 1u) ^ 1u);
+        mbar_arrive_expect_tx(&bar.q_full, 2 * kTile);
+        for (int h = 0; h < 2; ++h) {
+          const int tok = x.q0 + x.tok0 + h * bq_half;
+          tma_load_4d(smem + kOffQ + h * kTile, &tmQ, &bar.q_full, 0, 0, x.kvh, tok);
+          tma_load_4d(smem + kOffQ + h * kTile + kHalf, &tmQ, &bar.q_full, 64, 0, x.kvh, tok);
+        }
       }
-      // sub-blocks past the visible range are fetched at block index num_blocks: TMA zero-fills
       int id_next = (lane < nbt && lane < nsb_valid) ? __ldg(bt + lane / n16) : p.num_blocks;
       for (int jt = 0; jt < x.ntiles; ++jt) {
         const int id_cur = id_next;
         const int sb_next = (jt + 1) * nbt + lane;
         id_next = (jt + 1 < x.ntiles && lane < nbt && sb_next < nsb_valid) ? __ldg(bt + sb_next / n16) : p.num_blocks;
-        // K tile
-        {
-          const uint32_t s = kc % kStages, ph = (kc / kStages) & 1u;
+#pragma unroll
+        for (int kv = 0; kv < 2; ++kv) {
+          const CUtensorMap* tm = kv ? &tmV : &tmK;
+          const int nst = kv ? kVStages : kKStages;
+          uint32_t& cnt = kv ? vc : kc;
+          const uint32_t s = cnt % nst, ph = (cnt / nst) & 1u;
+          uint64_t* fullb = kv ? &bar.v_full[s] : &bar.k_full[s];
+          uint64_t* emptyb = kv ? &bar.v_empty[s] : &bar.k_empty[s];
+          uint8_t* base = smem + (kv ? kOffV : kOffK) + s * kTile;
           if (lane == 0) {
-            mbar_wait_tag(&bar.k_empty[s], ph ^ 1u, 2,(int)kc,it);
-            mbar_arrive_expect_tx(&bar.k_full[s], kTile);
+            mbar_wait(emptyb, ph ^ 1u);
+            mbar_arrive_expect_tx(fullb, kTile);
           }
           for (int i = 0; i < nbt; ++i) {
             const int blk = __shfl_sync(0xffffffffu, id_cur, i);
             const int slot0 = ((jt * nbt + i) % n16) * 16;
             const int c1 = p.kv_tok_inner ? slot0 : x.kvh, c2 = p.kv_tok_inner ? x.kvh : slot0;
             if (lane == 0) {
-              uint8_t* dst = smem + kOffK + s * kTile + i * 16 * 128;
-              tma_load_4d_hint(dst, &tmK, &bar.k_full[s], 0, c1, c2, blk, pol_kv);
-              tma_load_4d_hint(dst + kHalf, &tmK, &bar.k_full[s], 64, c1, c2, blk, pol_kv);
+              uint8_t* dst = base + i * 16 * 128;
+              tma_load_4d_hint(dst, tm, fullb, 0, c1, c2, blk, pol_kv);
+              tma_load_4d_hint(dst + kHalf, tm, fullb, 64, c1, c2, blk, pol_kv);
             }
           }
-          ++kc;
-        }
-        // V tile
-        {
-          const uint32_t s = vc % kStages, ph = (vc / kStages) & 1u;
-          if (lane == 0) {
-            mbar_wait_tag(&bar.v_empty[s], ph ^ 1u, 3,(int)vc,it);
-            mbar_arrive_expect_tx(&bar.v_full[s], kTile);
-          }
-          for (int i = 0; i < nbt; ++i) {
-            const int blk = __shfl_sync(0xffffffffu, id_cur, i);
-            const int slot0 = ((jt * nbt + i) % n16) * 16;
-            const int c1 = p.kv_tok_inner ? slot0 : x.kvh, c2 = p.kv_tok_inner ? x.kvh : slot0;
-            if (lane == 0) {
-              uint8_t* dst = smem + kOffV + s * kTile + i * 16 * 128;
-              tma_load_4d_hint(dst, &tmV, &bar.v_full[s], 0, c1, c2, blk, pol_kv);
-              tma_load_4d_hint(dst + kHalf, &tmV, &bar.v_full[s], 64, c1, c2, blk, pol_kv);
-            }
-          }
-          ++vc;
+          ++cnt;
         }
       }
     }
   } else if (warp == 1) {
     // ================================================================ MMA issuer (one thread)
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
     if (lane == 0) {
-      constexpr uint32_t idS = idesc_bf16_f32(kM, kN, 0, 0);   // Q (K-major) x K (K-major)
-      constexpr uint32_t idPV = idesc_bf16_f32(kM, kD, 0, 1);  // P (K-major) x V (MN-major)
-      uint32_t ic = 0, kc = 0, vc = 0, sc = 0, pc = 0;
-      auto issue_pv = [&](int t) {
-        mbar_wait_tag(&bar.p_full, pc & 1u, 11,(int)pc,t);
-        const uint32_t s = vc % kStages, ph = (vc / kStages) & 1u;
-        mbar_wait_tag(&bar.v_full[s], ph, 12,(int)vc,t);
-        if (t == 0) mbar_wait_tag(&bar.o_empty, (ic & 1u) ^ 1u, 13,(int)ic,t);
-        tc_fence_after();
-        const uint32_t pa = sbase + kOffP, va = sbase + kOffV + s * kTile;
-#pragma unroll
-        for (int k = 0; k < kN / 16; ++k) {
-          const uint64_t a = smem_desc_sw128(pa + (k >> 2) * kHalf + (k & 3) * 32, 16, 1024);
-          const uint64_t bdesc = smem_desc_sw128(va + k * 2048, kHalf, 1024);
-          tc_mma_f16_ss(tmem_O, a, bdesc, idPV, (t > 0 || k > 0) ? 1u : 0u);
-        }
-        tc_commit(&bar.pv_done);
-        tc_commit(&bar.v_empty[s]);
-        ++vc;
-        ++pc;
-      };
+      constexpr uint32_t idS = idesc_bf16_f32(kHalfM, kN, 0, 0);   // Q (K-major) x K (K-major)
+      constexpr uint32_t idPV = idesc_bf16_f32(kHalfM, kD, 0, 1);  // P (TMEM, K-major) x V (MN-major)
+      uint32_t ic = 0, kc = 0, vc = 0;
+      uint32_t pc[2] = {0u, 0u};
       for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++ic) {
         const Item x = prefill_item(p, total_qb, it);
-        mbar_wait_tag(&bar.q_full, ic & 1u, 14,(int)ic,it);
+        mbar_wait(&bar.q_full, ic & 1u);
         tc_fence_after();
-        for (int jt = 0; jt < x.ntiles; ++jt) {
-          const uint32_t s = kc % kStages, ph = (kc / kStages) & 1u;
-          const uint32_t sb = sc & 1u, sph = (sc >> 1) & 1u;
-          mbar_wait_tag(&bar.k_full[s], ph, 15,(int)kc,jt);
-          mbar_wait_tag(&bar.s_empty[sb], sph ^ 1u, 16,(int)sc,jt);
-          tc_fence_after();
-          const uint32_t qa = sbase + kOffQ, ka = sbase + kOffK + s * kTile;
-#pragma unroll
-          for (int k = 0; k < kD / 16; ++k) {
-            const uint32_t off = (k >> 2) * kHalf + (k & 3) * 32;
-            tc_mma_f16_ss(tmem_S0 + 128 * sb, smem_desc_sw128(qa + off, 16, 1024), smem_desc_sw128(ka + off, 16, 1024),
-                          idS, k > 0 ? 1u : 0u);
+        for (int jt = 0; jt <= x.ntiles; ++jt) {
+          const bool do_s = jt < x.ntiles, do_pv = jt > 0;
+          uint32_t ks = 0, vs = 0;
+          if (do_s) {
+            ks = kc % kKStages;
+            mbar_wait(&bar.k_full[ks], (kc / kKStages) & 1u);
           }
-          tc_commit(&bar.s_full[sb]);
-          tc_commit(&bar.k_empty[s]);
-          if (jt == x.ntiles - 1) tc_commit(&bar.q_empty);
-          ++kc;
-          ++sc;
-          if (jt > 0) issue_pv(jt - 1);
+          if (do_pv) {
+            vs = vc % kVStages;
+            mbar_wait(&bar.v_full[vs], (vc / kVStages) & 1u);
+          }
+          tc_fence_after();
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t tS = tmem + kTmemS + 128 * h, tO = tmem + kTmemO + 128 * h;
+            if (do_pv) {  // PV_h(jt-1): P_h aliases S_h, so it must precede S_h(jt)
+              mbar_wait(&bar.p_full[h], pc[h] & 1u);
+              if (jt == 1) mbar_wait(&bar.o_empty[h], (ic & 1u) ^ 1u);
+              tc_fence_after();
+              const uint32_t va = sbase + kOffV + vs * kTile;
+#pragma unroll
+              for (int k = 0; k < kN / 16; ++k)
+                tc_mma_f16_ts(tO, tS + 8 * k, smem_desc_sw128(va + k * 2048, kHalf, 1024), idPV,
+                              (jt > 1 || k > 0) ? 1u : 0u);
+              tc_commit(&bar.pv_done[h]);
+              ++pc[h];
+            }
+            if (do_s) {  // S_h(jt) = Q_h K^T
+              const uint32_t qa = sbase + kOffQ + h * kTile, ka = sbase + kOffK + ks * kTile;
+#pragma unroll
+              for (int k = 0; k < kD / 16; ++k) {
+                const uint32_t off = (k >> 2) * kHalf + (k & 3) * 32;
+                tc_mma_f16_ss(tS, smem_desc_sw128(qa + off, 16, 1024), smem_desc_sw128(ka + off, 16, 1024), idS,
+                              k > 0 ? 1u : 0u);
+              }
+              tc_commit(&bar.s_full[h]);
+            }
+          }
+          if (do_s) {
+            tc_commit(&bar.k_empty[ks]);
+            if (jt == x.ntiles - 1) tc_commit(&bar.q_empty);
+            ++kc;
+          }
+          if (do_pv) {
+            tc_commit(&bar.v_empty[vs]);
+            ++vc;
+          }
         }
-        issue_pv(x.ntiles - 1);
       }
     }
     __syncwarp();
-  } else if (warp >= 4) {
+  } else if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");  // idle warps of warpgroup 0
+  } else {
     // ================================================================ softmax / correction / epilogue
-    const int r = threadIdx.x - 128;  // row of the Q tile == TMEM lane
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;\n" ::: "memory");
+    const int h = (warp - 4) >> 2;             // half a (0) or b (1)
+    const int r = threadIdx.x - 128 - h * 128;  // row within the half == TMEM lane
     const uint32_t lane_off = (uint32_t)(32 * (warp & 3)) << 16;
-    const uint32_t pa = smem_u32(smem + kOffP);
-    uint32_t sc = 0, pc = 0, vc = 0;
+    const uint32_t tS = tmem + kTmemS + 128 * h + lane_off;
+    const uint32_t tO = tmem + kTmemO + 128 * h + lane_off;
+    uint32_t tc = 0, vc = 0;  // tiles seen by this warpgroup (== PV count of this half)
     __nv_bfloat16* O = static_cast<__nv_bfloat16*>(p.out);
+    const float cs = p.scale_log2;
+    const float ca = fmaxf(fabsf(cs), 1e-30f);  // scale 0: -inf * 0 would be NaN; 1e-30 * s ~ 0
     for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
       const Item x = prefill_item(p, total_qb, it);
-      const int tk = r / G;
+      const int tk = h * bq_half + r / G;  // token of this row within the Q block
       const bool row_valid = tk < x.ntok;
       const int row_lim = min(x.ctx + x.tok0 + tk + 1, x.kv_end);  // keys [0, row_lim) visible
-      const int nsb_valid = (x.kv_end + 15) / 16;  // 16-key sub-blocks fetched from the cache
+      const int nsb_valid = (x.kv_end + 15) / 16;                  // 16-key sub-blocks fetched
       float m_run = -INFINITY, l_run = 0.f;
       for (int jt = 0; jt < x.ntiles; ++jt) {
-        const uint32_t sb = sc & 1u, sph = (sc >> 1) & 1u;
-        mbar_wait_tag(&bar.s_full[sb], sph, 21,(int)sc,jt);
+        mbar_wait(&bar.s_full[h], tc & 1u);
         tc_fence_after();
         float s[kN];
         {
           uint32_t* su = reinterpret_cast<uint32_t*>(s);
-          const uint32_t ta = tmem_S0 + 128 * sb + lane_off;
-          PATTN_TMEM_LD32(ta + 0, (su + 0));
-          PATTN_TMEM_LD32(ta + 32, (su + 32));
-          PATTN_TMEM_LD32(ta + 64, (su + 64));
-          PATTN_TMEM_LD32(ta + 96, (su + 96));
+          PATTN_TMEM_LD32(tS + 0, (su + 0));
+          PATTN_TMEM_LD32(tS + 32, (su + 32));
+          PATTN_TMEM_LD32(tS + 64, (su + 64));
+          PATTN_TMEM_LD32(tS + 96, (su + 96));
           tmem_wait_ld();
         }
-        tc_fence_before();
-        mbar_arrive(&bar.s_empty[sb]);
-        ++sc;
-
         const int key0 = jt * kN;
         const int nvis = row_lim - key0;  // keys [key0, key0 + nvis) of this tile are visible
-        float mt = -INFINITY;
+        if (cs < 0.f) {  // sign-adjust so that max(raw) * |c| = max(scaled)
 #pragma unroll
-        for (int c = 0; c < kN; ++c) {
-          s[c] = c < nvis ? s[c] * p.scale_log2 : -INFINITY;
-          mt = fmaxf(mt, s[c]);
+          for (int c = 0; c < kN; ++c) s[c] = -s[c];
         }
+        if (__any_sync(0xffffffffu, nvis < kN)) {  // diagonal / tail tile: causal mask (warp-uniform)
+#pragma unroll
+          for (int c = 0; c < kN; ++c) s[c] = c < nvis ? s[c] : -INFINITY;
+        }
+        float mx[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) mx[i] = s[i];
+#pragma unroll
+        for (int c = 8; c < kN; ++c) mx[c & 7] = fmaxf(mx[c & 7], s[c]);
+        const float mraw = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                                 fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+        const float mt = mraw * ca;
         const float m_new = fmaxf(m_run, mt);
         float alpha = 1.f, m_use = m_run;
         if (m_new > m_run + kRescaleThreshold) {  // includes m_run == -inf
           alpha = fast_exp2(m_run - m_new);
           m_use = m_new;
         }
-        const float base = m_use == -INFINITY ? 0.f : m_use;
-        float rs = 0.f;
+        const float nbase = m_use == -INFINITY ? 0.f : -m_use;
+        float rsv[8];
 #pragma unroll
-        for (int c = 0; c < kN; ++c) {
-          s[c] = fast_exp2(s[c] - base);
-          rs += s[c];
+        for (int i = 0; i < 8; ++i) rsv[i] = 0.f;
+        uint32_t pk[kN / 2];
+#pragma unroll
+        for (int c = 0; c < kN; c += 2) {
+          const float e0 = fast_exp2(fmaf(s[c], ca, nbase));  // e^{scale*qk - m}, log2 domain
+          const float e1 = fast_exp2(fmaf(s[c + 1], ca, nbase));
+          rsv[c & 7] += e0;
+          rsv[(c + 1) & 7] += e1;
+          pk[c >> 1] = pack_bf16(e0, e1);
         }
-        // PV of the previous tile must be done before P (smem) and O (TMEM) are touched
+        const float rs = ((rsv[0] + rsv[1]) + (rsv[2] + rsv[3])) + ((rsv[4] + rsv[5]) + (rsv[6] + rsv[7]));
+        // O_h: PV_h(jt-1) was issued before S_h(jt) (in-order), so it is complete; the barrier
+        // wait orders its TMEM writes before our correction.
         if (jt > 0) {
-          mbar_wait_tag(&bar.pv_done, (pc - 1) & 1u, 22,(int)pc,jt);
+          mbar_wait(&bar.pv_done[h], (tc - 1) & 1u);
           tc_fence_after();
           // tcgen05.ld/st are warp-collective (.sync.aligned): rescale when ANY row of the warp needs it
           if (__any_sync(0xffffffffu, alpha != 1.f)) {
 #pragma unroll
             for (int c0 = 0; c0 < kD; c0 += 32) {
               uint32_t o[32];
-              PATTN_TMEM_LD32(tmem_O + lane_off + c0, o);
+              PATTN_TMEM_LD32(tO + c0, o);
               tmem_wait_ld();
 #pragma unroll
               for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * alpha);
-              PATTN_TMEM_ST32(tmem_O + lane_off + c0, o);
+              PATTN_TMEM_ST32(tO + c0, o);
             }
-            tmem_wait_st();
           }
         }
         l_run = l_run * alpha + rs;
         m_run = m_use;
-        // P row (bf16) -> shared memory, UMMA K-major SW128: [key half][row][128 B], chunk ^= row & 7
-#pragma unroll
-        for (int ch = 0; ch < kN / 8; ++ch) {
-          uint4 v;
-          v.x = pack_bf16(s[ch * 8 + 0], s[ch * 8 + 1]);
-          v.y = pack_bf16(s[ch * 8 + 2], s[ch * 8 + 3]);
-          v.z = pack_bf16(s[ch * 8 + 4], s[ch * 8 + 5]);
-          v.w = pack_bf16(s[ch * 8 + 6], s[ch * 8 + 7]);
-          const uint32_t addr = pa + (ch >> 3) * kHalf + r * 128 + (((ch & 7) ^ (r & 7)) << 4);
-          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z),
-                       "r"(v.w)
-                       : "memory");
-        }
-        // zero V rows of slots >= L inside the last valid paged block (may hold NaN)
-        const int z0 = x.L - key0, z1 = min(kN, nsb_valid * 16 - key0);
-        if (z0 < z1 && z0 < kN) {
-          const uint32_t s2 = vc % kStages, ph2 = (vc / kStages) & 1u;
-          mbar_wait_tag(&bar.v_full[s2], ph2, 23,(int)vc,jt);
-          uint8_t* vb = smem + kOffV + s2 * kTile;
-          const int zs = max(z0, 0);
-          for (int e = r; e < (z1 - zs) * 16; e += kM) {
-            const int row = zs + (e >> 4), ch = e & 15;
-            *reinterpret_cast<uint4*>(vb + (ch >> 3) * kHalf + row * 128 + ((ch & 7) << 4)) = make_uint4(0, 0, 0, 0);
+        // P (bf16, 2 per column) over the first 64 columns of S_h: the A operand of PV_h
+        PATTN_TMEM_ST32(tS + 0, (pk + 0));
+        PATTN_TMEM_ST32(tS + 32, (pk + 32));
+        // WG a: zero V rows of slots >= L inside the last fetched sub-block (they may hold NaN)
+        if (h == 0) {
+          const int z0 = x.L - key0, z1 = min(kN, nsb_valid * 16 - key0);
+          if (z0 < z1 && z0 < kN) {
+            const uint32_t s2 = vc % kVStages;
+            mbar_wait(&bar.v_full[s2], (vc / kVStages) & 1u);
+            uint8_t* vb = smem + kOffV + s2 * kTile;
+            for (int e = r; e < (z1 - z0) * 16; e += kHalfM) {
+              const int row = z0 + (e >> 4), ch = e & 15;
+              *reinterpret_cast<uint4*>(vb + (ch >> 3) * kHalf + row * 128 + ((ch & 7) << 4)) = make_uint4(0, 0, 0, 0);
+            }
+            fence_proxy_async_smem();
           }
         }
         ++vc;
-        fence_proxy_async_smem();
+        tmem_wait_st();
         tc_fence_before();
-        mbar_arrive(&bar.p_full);
-        ++pc;
+        mbar_arrive(&bar.p_full[h]);
+        ++tc;
       }
       // ---- epilogue: O / l -> bf16 -> out (valid rows only)
-      mbar_wait_tag(&bar.pv_done, (pc - 1) & 1u, 24,(int)pc,it);
+      mbar_wait(&bar.pv_done[h], (tc - 1) & 1u);
       tc_fence_after();
       const float inv = 1.f / l_run;
-      __nv_bfloat16* orow = O + (int64_t)(x.q0 + x.tok0 + tk) * p.o_st_tok + (int64_t)(x.kvh * G + (r - tk * G)) * p.o_st_head;
+      __nv_bfloat16* orow =
+          O + (int64_t)(x.q0 + x.tok0 + tk) * p.o_st_tok + (int64_t)(x.kvh * G + (r % G)) * p.o_st_head;
 #pragma unroll
       for (int c0 = 0; c0 < kD; c0 += 32) {
         uint32_t o[32];
-        PATTN_TMEM_LD32(tmem_O + lane_off + c0, o);
+        PATTN_TMEM_LD32(tO + c0, o);
         tmem_wait_ld();
         if (row_valid) {
 #pragma unroll
@@ -364,7 +399,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       tc_fence_before();
-      mbar_arrive(&bar.o_empty);
+      mbar_arrive(&bar.o_empty[h]);
     }
   }
 
@@ -378,8 +413,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 bool prefill_supported(const Params& p) {
   if (getenv("PATTN_DISABLE_K1")) return false;
-  return p.D == kD && p.G >= 1 && p.G <= kM && (kM % p.G) == 0 && p.bs % 16 == 0;
+  // BLOCK_Q = 256/G tokens split into two halves of 128 rows: G must divide 128
+  return p.D == kD && p.G >= 1 && p.G <= kHalfM && (kHalfM % p.G) == 0 && p.bs % 16 == 0;
 }
+
+int prefill_block_q(int G) { return kM / G; }
 
 PrefillLaunch plan_prefill(const Params& p, int num_sms) {
   PrefillLaunch pl;

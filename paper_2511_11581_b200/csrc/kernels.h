@@ -35,6 +35,7 @@ struct PrefillLaunch {
   size_t smem;
 };
 bool prefill_supported(const Params& p);
+int prefill_block_q(int G);  // tokens per K1 Q block (BLOCK_M / G)
 PrefillLaunch plan_prefill(const Params& p, int num_sms);
 cudaError_t launch_prefill(const Params& p, const PrefillLaunch& pl, const CUtensorMap& tmQ, const CUtensorMap& tmK,
                            const CUtensorMap& tmV, cudaStream_t stream);

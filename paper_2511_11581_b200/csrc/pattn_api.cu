@@ -162,7 +162,7 @@ pattn_status_t make_plan(const pattn_problem_t* p, const void* q, const void* kc
   const int max_q = p->max_query_len > 0 ? p->max_query_len : p->num_tokens;
   const bool maybe_prefill = max_q > 1 || !pl->use_k2;
   if (pl->use_k1) {
-    pl->block_q = std::max(1, 128 / G);
+    pl->block_q = prefill_block_q(G);  // BLOCK_M = 256 rows = BLOCK_Q tokens x G heads
     pl->use_k1 = maybe_prefill;
   } else {
     pl->block_q = G <= 32 ? std::max(1, 32 / G) : 1;
@@ -263,7 +263,7 @@ bool encode_q_map(CUtensorMap* tm, const pattn_problem_t* p, const void* q, int 
                         (cuuint64_t)std::max(1, p->num_tokens)};
   cuuint64_t strides[3] = {(cuuint64_t)p->q_stride_head * 2, (cuuint64_t)p->q_stride_head * 2 * G,
                            (cuuint64_t)p->q_stride_tok * 2};
-  cuuint32_t box[4] = {64, (cuuint32_t)G, 1, (cuuint32_t)block_q};
+  cuuint32_t box[4] = {64, (cuuint32_t)G, 1, (cuuint32_t)(block_q / 2)};  // one 128-row half
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(q), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
