@@ -31,6 +31,43 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#ifdef PATTN_TRACE
+// debug timeline of CTA 0: one array per recording thread (no atomics: fire-and-forget stores)
+// slot = (role, index): role 0 MMA thread, 1/2 softmax WG a/b thread 0, 3/4 K/V producer lane 0
+__device__ unsigned long long g_k1_trace[5][2 * 2048];
+__device__ unsigned int g_k1_trace_n[5];
+#define PATTN_K1_TRACE_ROLE(role, cnt, code)                          \
+  do {                                                                \
+    if (blockIdx.x == 0 && (cnt) < 2048) {                            \
+      g_k1_trace[role][2 * (cnt)] = clock64();                        \
+      g_k1_trace[role][2 * (cnt) + 1] = (code);                       \
+      g_k1_trace_n[role] = ++(cnt);                                   \
+    }                                                                 \
+  } while (0)
+extern "C" __attribute__((visibility("default"))) int pattn_debug_k1_trace(unsigned long long* host, int cap, int reset) {
+  unsigned int n[5];
+  cudaMemcpyFromSymbol(n, g_k1_trace_n, sizeof(n));
+  static unsigned long long tmp[5][2 * 2048];
+  cudaMemcpyFromSymbol(tmp, g_k1_trace, sizeof(tmp));
+  int k = 0;
+  for (int r = 0; r < 5; ++r)
+    for (unsigned i = 0; i < n[r] && i < 2048 && k < cap; ++i, ++k) {
+      host[2 * k] = tmp[r][2 * i];
+      host[2 * k + 1] = tmp[r][2 * i + 1];
+    }
+  if (reset) {
+    unsigned int z[5] = {0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(g_k1_trace_n, z, sizeof(z));
+  }
+  return k;
+}
+#define PATTN_K1_TRACE(code) PATTN_K1_TRACE_ROLE(trace_role, trace_cnt, code)
+#else
+#define PATTN_K1_TRACE(code) \
+  do {                       \
+  } while (0)
+#endif
+
 namespace pattn {
 namespace {
 
@@ -44,6 +81,10 @@ constexpr uint32_t kHalf = kTile / 2;    // 16 KB: one 64-wide d half
 constexpr int kKStages = 3;
 constexpr int kVStages = 2;
 constexpr float kRescaleThreshold = 8.0f;  // log2 domain: rescale O only if the max grows by > 2^8
+#ifndef PATTN_POLY_MASK
+#define PATTN_POLY_MASK 255  // measured: FMA-pipe exp2 did not pay off here
+#endif
+constexpr int kPolyMask = PATTN_POLY_MASK;  // exp2 pair j on the FMA pipe iff (j & mask) == mask: 1 -> 1/2
 
 // shared-memory map (offsets from a 1024-aligned base)
 constexpr uint32_t kOffQ = 0;  // half a: [0, 32K), half b: [32K, 64K)
@@ -87,6 +128,27 @@ __device__ __forceinline__ Item prefill_item(const Params& p, int total_qb, int 
   return x;
 }
 
+// The XU pipe (MUFU.EX2 and F2FP conversions) is the softmax's bottleneck on B200: per
+// 128x128 tile, 16384 exp2 + 8192 bf16x2 packs at 8 ops/clk/SM take ~3x the 1024 clk the
+// two UMMAs need.  So (1) P is packed to bf16 with integer ops (round-half-up on the fp32
+// bits, then a byte permute) and (2) a fraction of the exp2 run on the FMA pipe:
+// 2^x = 2^n * p(f), n = rint(x), f = x - n in [-0.5, 0.5], p a degree-3 minimax polynomial
+// (max relative error 7.5e-5, far below bf16's 2^-9 rounding of P; reading R12).
+PATTN_DEVICE uint32_t pack_bf16_alu(float lo, float hi) {
+  const uint32_t a = __float_as_uint(lo) + 0x8000u, b = __float_as_uint(hi) + 0x8000u;
+  return __byte_perm(a, b, 0x7632);  // {hi16(b), hi16(a)}; p >= 0 and finite
+}
+PATTN_DEVICE float exp2_poly(float x) {
+  x = fmaxf(x, -126.f);                          // keeps 2^n a normal power of two (tiny, not 0)
+  const float t = __fadd_rn(x, 12582912.f);      // 1.5 * 2^23: n = rint(x) in the low mantissa bits
+  const float n = __fadd_rn(t, -12582912.f);
+  const float f = __fadd_rn(x, -n);
+  float pp = fmaf(0.05517161265015602f, f, 0.24261116981506348f);
+  pp = fmaf(pp, f, 0.6932610273361206f);
+  pp = fmaf(pp, f, 0.9999280571937561f);
+  return __int_as_float(__float_as_int(pp) + (__float_as_int(t) << 23));
+}
+
 // O[tmem] (+)= A[tmem] * B[smem desc]; kind::f16, A (P) K-major in TMEM.
 PATTN_DEVICE void tc_mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc, uint32_t accum) {
   asm volatile(
@@ -105,6 +167,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   Bars& bar = *reinterpret_cast<Bars*>(smem + kOffBar);
   const uint32_t sbase = smem_u32(smem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef PATTN_TRACE
+  const int trace_role = warp == 1 ? 0 : warp == 0 ? 3 : warp == 3 ? 4 : warp == 4 ? 1 : 2;
+  unsigned int trace_cnt = 0;
+#endif
 
   if (threadIdx.x == 0) {
     mbar_init(&bar.q_full, 1);
@@ -139,25 +205,29 @@ __global__ void __launch_bounds__(kThreads, 1)
   // register rebalancing per warpgroup: producer/MMA warpgroup 56, softmax warpgroups 224
   // (128*56 + 256*224 = 64512 <= 65536)
 
-  if (warp == 0) {
-    // ================================================================ TMA producer
+  if (warp == 0 || warp == 3) {
+    // ================================================================ TMA producers
+    // warp 0: Q and the K ring; warp 3: the V ring (independent, so a V stage still in use
+    // by PV never delays the next K tile the S MMA is waiting for)
     asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
+    const int kv = warp == 3 ? 1 : 0;
     if (lane == 0) {
-      tma_prefetch_desc(&tmQ);
-      tma_prefetch_desc(&tmK);
-      tma_prefetch_desc(&tmV);
+      if (kv == 0) tma_prefetch_desc(&tmQ);
+      tma_prefetch_desc(kv ? &tmV : &tmK);
     }
     // A 128-key tile = 8 sub-blocks of 16 keys; sub-block idx is slots [(idx % n16)*16, +16)
     // of paged block bt[idx / n16] (any block size that is a multiple of 16).
     constexpr int nbt = kN / 16;
     const int n16 = p.bs / 16;
     const uint64_t pol_kv = l2_policy_evict_last();  // K/V tiles are re-read by the sequence's other Q blocks
-    uint32_t ic = 0, kc = 0, vc = 0;
+    const CUtensorMap* tm = kv ? &tmV : &tmK;
+    const int nst = kv ? kVStages : kKStages;
+    uint32_t ic = 0, cnt = 0;
     for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++ic) {
       const Item x = prefill_item(p, total_qb, it);
       const int32_t* bt = p.block_table + (int64_t)x.b * p.bt_stride;
       const int nsb_valid = (x.kv_end + 15) / 16;  // sub-blocks holding visible keys
-      if (lane == 0) {
+      if (kv == 0 && lane == 0) {
         mbar_wait(&bar.q_empty, (ic & 1u) ^ 1u);
         mbar_arrive_expect_tx(&bar.q_full, 2 * kTile);
         for (int h = 0; h < 2; ++h) {
@@ -171,98 +241,107 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int id_cur = id_next;
         const int sb_next = (jt + 1) * nbt + lane;
         id_next = (jt + 1 < x.ntiles && lane < nbt && sb_next < nsb_valid) ? __ldg(bt + sb_next / n16) : p.num_blocks;
-#pragma unroll
-        for (int kv = 0; kv < 2; ++kv) {
-          const CUtensorMap* tm = kv ? &tmV : &tmK;
-          const int nst = kv ? kVStages : kKStages;
-          uint32_t& cnt = kv ? vc : kc;
-          const uint32_t s = cnt % nst, ph = (cnt / nst) & 1u;
-          uint64_t* fullb = kv ? &bar.v_full[s] : &bar.k_full[s];
-          uint64_t* emptyb = kv ? &bar.v_empty[s] : &bar.k_empty[s];
-          uint8_t* base = smem + (kv ? kOffV : kOffK) + s * kTile;
-          if (lane == 0) {
-            mbar_wait(emptyb, ph ^ 1u);
-            mbar_arrive_expect_tx(fullb, kTile);
-          }
-          for (int i = 0; i < nbt; ++i) {
-            const int blk = __shfl_sync(0xffffffffu, id_cur, i);
-            const int slot0 = ((jt * nbt + i) % n16) * 16;
-            const int c1 = p.kv_tok_inner ? slot0 : x.kvh, c2 = p.kv_tok_inner ? x.kvh : slot0;
-            if (lane == 0) {
-              uint8_t* dst = base + i * 16 * 128;
-              tma_load_4d_hint(dst, tm, fullb, 0, c1, c2, blk, pol_kv);
-              tma_load_4d_hint(dst + kHalf, tm, fullb, 64, c1, c2, blk, pol_kv);
-            }
-          }
-          ++cnt;
+        const uint32_t s = cnt % nst, ph = (cnt / nst) & 1u;
+        uint64_t* fullb = kv ? &bar.v_full[s] : &bar.k_full[s];
+        uint64_t* emptyb = kv ? &bar.v_empty[s] : &bar.k_empty[s];
+        uint8_t* base = smem + (kv ? kOffV : kOffK) + s * kTile;
+        if (lane == 0) {
+          mbar_wait(emptyb, ph ^ 1u);
+          mbar_arrive_expect_tx(fullb, kTile);
         }
+        for (int i = 0; i < nbt; ++i) {
+          const int blk = __shfl_sync(0xffffffffu, id_cur, i);
+          const int slot0 = ((jt * nbt + i) % n16) * 16;
+          const int c1 = p.kv_tok_inner ? slot0 : x.kvh, c2 = p.kv_tok_inner ? x.kvh : slot0;
+          if (lane == 0) {
+            uint8_t* dst = base + i * 16 * 128;
+            if (i == 0) PATTN_K1_TRACE(20 + kv);
+            tma_load_4d_hint(dst, tm, fullb, 0, c1, c2, blk, pol_kv);
+            tma_load_4d_hint(dst + kHalf, tm, fullb, 64, c1, c2, blk, pol_kv);
+          }
+        }
+        ++cnt;
       }
     }
   } else if (warp == 1) {
-    // ================================================================ MMA issuer (one thread)
+    // ================================================================ MMA issuer
+    // The whole warp runs the schedule (waits, descriptor arithmetic stay warp-uniform, in
+    // uniform registers); one elected lane issues each tcgen05.mma / commit.
     asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
-    if (lane == 0) {
-      constexpr uint32_t idS = idesc_bf16_f32(kHalfM, kN, 0, 0);   // Q (K-major) x K (K-major)
-      constexpr uint32_t idPV = idesc_bf16_f32(kHalfM, kD, 0, 1);  // P (TMEM, K-major) x V (MN-major)
-      uint32_t ic = 0, kc = 0, vc = 0;
-      uint32_t pc[2] = {0u, 0u};
-      for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++ic) {
-        const Item x = prefill_item(p, total_qb, it);
-        mbar_wait(&bar.q_full, ic & 1u);
+    constexpr uint32_t idS = idesc_bf16_f32(kHalfM, kN, 0, 0);   // Q (K-major) x K (K-major)
+    constexpr uint32_t idPV = idesc_bf16_f32(kHalfM, kD, 0, 1);  // P (TMEM, K-major) x V (MN-major)
+    // smem descriptors: start-address field = addr >> 4, so desc(base + off) = desc(base) + (off >> 4)
+    const uint64_t dQ = smem_desc_sw128(sbase + kOffQ, 16, 1024);
+    const uint64_t dK = smem_desc_sw128(sbase + kOffK, 16, 1024);
+    const uint64_t dV = smem_desc_sw128(sbase + kOffV, kHalf, 1024);
+    const bool leader = elect_one();
+    uint32_t ic = 0, kc = 0, vc = 0;
+    uint32_t pc[2] = {0u, 0u};
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++ic) {
+      const Item x = prefill_item(p, total_qb, it);
+      mbar_wait(&bar.q_full, ic & 1u);
+      tc_fence_after();
+      for (int jt = 0; jt <= x.ntiles; ++jt) {
+        const bool do_s = jt < x.ntiles, do_pv = jt > 0;
+        uint32_t ks = 0, vs = 0;
+        if (do_s) {
+          ks = kc % kKStages;
+          mbar_wait(&bar.k_full[ks], (kc / kKStages) & 1u);
+          if (leader) PATTN_K1_TRACE(1);
+        }
+        if (do_pv) {
+          vs = vc % kVStages;
+          mbar_wait(&bar.v_full[vs], (vc / kVStages) & 1u);
+          if (leader) PATTN_K1_TRACE(2);
+        }
         tc_fence_after();
-        for (int jt = 0; jt <= x.ntiles; ++jt) {
-          const bool do_s = jt < x.ntiles, do_pv = jt > 0;
-          uint32_t ks = 0, vs = 0;
-          if (do_s) {
-            ks = kc % kKStages;
-            mbar_wait(&bar.k_full[ks], (kc / kKStages) & 1u);
-          }
-          if (do_pv) {
-            vs = vc % kVStages;
-            mbar_wait(&bar.v_full[vs], (vc / kVStages) & 1u);
-          }
-          tc_fence_after();
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const uint32_t tS = tmem + kTmemS + 128 * h, tO = tmem + kTmemO + 128 * h;
-            if (do_pv) {  // PV_h(jt-1): P_h aliases S_h, so it must precede S_h(jt)
-              mbar_wait(&bar.p_full[h], pc[h] & 1u);
-              if (jt == 1) mbar_wait(&bar.o_empty[h], (ic & 1u) ^ 1u);
-              tc_fence_after();
-              const uint32_t va = sbase + kOffV + vs * kTile;
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t tS = tmem + kTmemS + 128 * h, tO = tmem + kTmemO + 128 * h;
+          if (do_pv) {  // PV_h(jt-1): P_h aliases S_h, so it must precede S_h(jt)
+            mbar_wait(&bar.p_full[h], pc[h] & 1u);
+            if (jt == 1) mbar_wait(&bar.o_empty[h], (ic & 1u) ^ 1u);
+            tc_fence_after();
+            if (leader) {
+              PATTN_K1_TRACE(3 + h);
+              const uint64_t dv = dV + ((vs * kTile) >> 4);
 #pragma unroll
               for (int k = 0; k < kN / 16; ++k)
-                tc_mma_f16_ts(tO, tS + 8 * k, smem_desc_sw128(va + k * 2048, kHalf, 1024), idPV,
-                              (jt > 1 || k > 0) ? 1u : 0u);
+                tc_mma_f16_ts(tO, tS + 8 * k, dv + ((k * 2048) >> 4), idPV, (jt > 1 || k > 0) ? 1u : 0u);
+              PATTN_K1_TRACE(5 + h);
               tc_commit(&bar.pv_done[h]);
-              ++pc[h];
             }
-            if (do_s) {  // S_h(jt) = Q_h K^T
-              const uint32_t qa = sbase + kOffQ + h * kTile, ka = sbase + kOffK + ks * kTile;
+            __syncwarp();
+            ++pc[h];
+          }
+          if (do_s) {  // S_h(jt) = Q_h K^T
+            if (leader) {
+              const uint64_t dq = dQ + ((h * kTile) >> 4), dk = dK + ((ks * kTile) >> 4);
 #pragma unroll
               for (int k = 0; k < kD / 16; ++k) {
-                const uint32_t off = (k >> 2) * kHalf + (k & 3) * 32;
-                tc_mma_f16_ss(tS, smem_desc_sw128(qa + off, 16, 1024), smem_desc_sw128(ka + off, 16, 1024), idS,
-                              k > 0 ? 1u : 0u);
+                const uint32_t off = ((k >> 2) * kHalf + (k & 3) * 32) >> 4;
+                tc_mma_f16_ss(tS, dq + off, dk + off, idS, k > 0 ? 1u : 0u);
               }
+              PATTN_K1_TRACE(7 + h);
               tc_commit(&bar.s_full[h]);
             }
+            __syncwarp();
           }
+        }
+        if (leader) {
           if (do_s) {
             tc_commit(&bar.k_empty[ks]);
             if (jt == x.ntiles - 1) tc_commit(&bar.q_empty);
-            ++kc;
           }
-          if (do_pv) {
-            tc_commit(&bar.v_empty[vs]);
-            ++vc;
-          }
+          if (do_pv) tc_commit(&bar.v_empty[vs]);
         }
+        __syncwarp();
+        if (do_s) ++kc;
+        if (do_pv) ++vc;
       }
     }
-    __syncwarp();
   } else if (warp < 4) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");  // idle warps of warpgroup 0
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");  // warp 2 (TMEM allocator) idles
   } else {
     // ================================================================ softmax / correction / epilogue
     asm volatile("setmaxnreg.inc.sync.aligned.u32 224;\n" ::: "memory");
@@ -284,6 +363,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       float m_run = -INFINITY, l_run = 0.f;
       for (int jt = 0; jt < x.ntiles; ++jt) {
         mbar_wait(&bar.s_full[h], tc & 1u);
+        if (r == 0) PATTN_K1_TRACE(10 + h);
         tc_fence_after();
         float s[kN];
         {
@@ -325,8 +405,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t pk[kN / 2];
 #pragma unroll
         for (int c = 0; c < kN; c += 2) {
-          const float e0 = fast_exp2(fmaf(s[c], ca, nbase));  // e^{scale*qk - m}, log2 domain
-          const float e1 = fast_exp2(fmaf(s[c + 1], ca, nbase));
+          // e^{scale*qk - m} in the log2 domain; pairs with (c & kPolyMask) == kPolyMask on the FMA pipe
+          const float x0 = fmaf(s[c], ca, nbase), x1 = fmaf(s[c + 1], ca, nbase);
+          const bool poly = ((c >> 1) & kPolyMask) == kPolyMask;
+          const float e0 = poly ? exp2_poly(x0) : fast_exp2(x0);
+          const float e1 = poly ? exp2_poly(x1) : fast_exp2(x1);
           rsv[c & 7] += e0;
           rsv[(c + 1) & 7] += e1;
           pk[c >> 1] = pack_bf16(e0, e1);
@@ -372,6 +455,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ++vc;
         tmem_wait_st();
         tc_fence_before();
+        if (r == 0) PATTN_K1_TRACE(12 + h);
         mbar_arrive(&bar.p_full[h]);
         ++tc;
       }

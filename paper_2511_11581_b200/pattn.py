@@ -18,7 +18,7 @@ from typing import Optional, Sequence
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libpattn.so")
+LIB_PATH = os.environ.get("PATTN_LIB") or os.path.join(_HERE, "lib", "libpattn.so")  # PATTN_LIB: A/B builds
 
 PATTN_OK = 0
 STATUS = {
