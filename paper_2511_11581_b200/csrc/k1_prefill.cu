@@ -78,8 +78,8 @@ constexpr int kD = 128;        // head dim
 constexpr int kThreads = 384;  // 12 warps
 constexpr uint32_t kTile = kN * kD * 2;  // 32 KB: one bf16 128x128 tile
 constexpr uint32_t kHalf = kTile / 2;    // 16 KB: one 64-wide d half
-constexpr int kKStages = 3;
-constexpr int kVStages = 2;
+constexpr int kKStages = 2;
+constexpr int kVStages = 3;  // V waits on PV (later than S), so it gets the deeper ring
 constexpr float kRescaleThreshold = 8.0f;  // log2 domain: rescale O only if the max grows by > 2^8
 #ifndef PATTN_POLY_MASK
 #define PATTN_POLY_MASK 255  // measured: FMA-pipe exp2 did not pay off here

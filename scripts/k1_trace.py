@@ -38,7 +38,7 @@ ev = ev[np.argsort(ev[:, 0], kind="stable")]
 ev = ev[ev[:, 0] > 0]
 t0 = ev[0, 0]
 names = {1: "K_ready", 2: "V_ready", 3: "Pa_ready", 4: "Pb_ready", 5: "PVa_issued", 6: "PVb_issued", 7: "Sa_issued",
-         8: "Sb_issued", 10: "SMa_start", 11: "SMb_start", 12: "SMa_done", 13: "SMb_done", 20: "K_load", 21: "V_load"}
+         8: "Sb_issued", 10: "SMa_start", 11: "SMb_start", 12: "SMa_done", 13: "SMb_done", 20: "K_load", 21: "V_load", 22: "K_issued", 23: "V_issued"}
 print("events", n)
 for t, c in ev[:160]:
     print(f"{int(t - t0):8d}  {names.get(int(c), c)}")
@@ -52,3 +52,23 @@ sa = ev[ev[:, 1] == 10, 0].astype(np.int64)
 da = ev[ev[:, 1] == 12, 0].astype(np.int64)
 m = min(len(sa), len(da))
 print("softmax a duration median", np.median(da[:m] - sa[:m]))
+# where does the MMA thread wait?  gap from the previous MMA event to each readiness event
+mma_codes = {1, 2, 3, 4, 5, 6, 7, 8}
+mm = ev[np.isin(ev[:, 1], list(mma_codes))]
+gaps = {}
+for i in range(1, len(mm)):
+    c = int(mm[i, 1])
+    gaps.setdefault(c, []).append(int(mm[i, 0]) - int(mm[i - 1, 0]))
+for c, g in sorted(gaps.items()):
+    print(f"MMA gap before {names[c]:12s} median {np.median(g):7.0f} mean {np.mean(g):7.0f}")
+
+for a, b, nm in ((20, 22, "K"), (21, 23, "V")):
+    ta = ev[ev[:, 1] == a, 0].astype(np.int64)
+    tb = ev[ev[:, 1] == b, 0].astype(np.int64)
+    m = min(len(ta), len(tb))
+    print(f"{nm} producer: issue duration median {np.median(tb[:m] - ta[:m]):7.0f}")
+ka = ev[ev[:, 1] == 22, 0].astype(np.int64)
+kr = ev[ev[:, 1] == 1, 0].astype(np.int64)
+# K tile j issued (ka[j]) -> MMA observed K ready (kr[j])
+m = min(len(ka), len(kr))
+print("K issued->ready median", np.median(kr[:m] - ka[:m]))
