@@ -8,8 +8,9 @@
 //     M = max_s m_s ;  w_s = 2^{m_s - M} (0 for an empty segment, m_s = -inf)
 //     out[h][:] = sum_s w_s acc_s[:] / sum_s w_s l_s
 // Segments are combined in index order (deterministic; no atomics).
-// Grid: (num_seqs, Hkv * HG); each CTA handles the <= 8 query heads of one
-// (sequence, KV head, head group); non-decode or unsplit sequences exit at once.
+// Grid: (num_seqs, Hkv * HG, D / 32); each 64-thread CTA handles 32 head-dim lanes of the
+// <= 8 query heads of one (sequence, KV head, head group); non-decode or unsplit sequences
+// exit at once.
 #include "common.cuh"
 #include "kernels.h"
 
@@ -17,7 +18,7 @@ namespace pattn {
 namespace {
 
 template <int D>
-__global__ void __launch_bounds__(128) k3_reduce(Params p) {
+__global__ void __launch_bounds__(64) k3_reduce(Params p) {
   const int b = blockIdx.x;
   const int qb = p.cu_seqlens_q[b + 1] - p.cu_seqlens_q[b];
   if (!(p.decode_to_k2 && qb == 1)) return;
@@ -28,11 +29,10 @@ __global__ void __launch_bounds__(128) k3_reduce(Params p) {
   const int g_eff = min(8, p.G - hg * 8);
   const int head0 = kvh * p.G + hg * 8;
   const int tok = p.cu_seqlens_q[b];
-  constexpr int D4 = D / 4;
   __nv_bfloat16* O = static_cast<__nv_bfloat16*>(p.out);
-  for (int idx = threadIdx.x; idx < g_eff * D4; idx += blockDim.x) {
-    const int h = head0 + idx / D4;
-    const int d4 = idx % D4;
+  for (int idx = threadIdx.x; idx < g_eff * 8; idx += blockDim.x) {
+    const int h = head0 + idx / 8;
+    const int d4 = blockIdx.z * 8 + idx % 8;
     float M = -INFINITY;
     for (int c = 0; c < n; ++c) M = fmaxf(M, p.part_m[(int64_t)(c0 + c) * p.Hq + h]);
     float den = 0.f;
@@ -59,11 +59,11 @@ __global__ void __launch_bounds__(128) k3_reduce(Params p) {
 }  // namespace
 
 cudaError_t launch_reduce(const Params& p, cudaStream_t stream) {
-  dim3 grid(p.B, p.Hkv * p.HG);
+  dim3 grid(p.B, p.Hkv * p.HG, p.D / 32);
   if (p.D == 64)
-    k3_reduce<64><<<grid, 128, 0, stream>>>(p);
+    k3_reduce<64><<<grid, 64, 0, stream>>>(p);
   else if (p.D == 128)
-    k3_reduce<128><<<grid, 128, 0, stream>>>(p);
+    k3_reduce<128><<<grid, 64, 0, stream>>>(p);
   else
     return cudaErrorInvalidValue;
   return cudaGetLastError();

@@ -181,7 +181,7 @@ pattn_status_t make_plan(const pattn_problem_t* p, const void* q, const void* kc
     pl->target_items = pl->num_sms * 64;
     pl->min_chunk = 1;
   } else {
-    pl->target_items = env_int("PATTN_TARGET_ITEMS", pl->num_sms * 8);
+    pl->target_items = env_int("PATTN_TARGET_ITEMS", pl->num_sms * 16);
     pl->min_chunk = env_int("PATTN_MIN_CHUNK_BLOCKS", std::max(1, 256 / p->block_size));
   }
   if (pl->target_items < 1) pl->target_items = 1;
