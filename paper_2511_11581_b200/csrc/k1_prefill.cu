@@ -205,12 +205,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   // register rebalancing per warpgroup: producer/MMA warpgroup 56, softmax warpgroups 224
   // (128*56 + 256*224 = 64512 <= 65536)
 
-  if (warp == 0 || warp == 3) {
+  if (warp == 0 || warp == 2 || warp == 3) {
     // ================================================================ TMA producers
-    // warp 0: Q and the K ring; warp 3: the V ring (independent, so a V stage still in use
-    // by PV never delays the next K tile the S MMA is waiting for)
+    // warp 0: Q and sub-blocks 0-3 of every K tile, warp 2: K sub-blocks 4-7, warp 3: the V
+    // ring.  K and V rings are independent (a V stage still in use by PV never delays the
+    // next K tile the S MMA waits for) and the per-box TMA issue cost is spread over warps.
     asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
     const int kv = warp == 3 ? 1 : 0;
+    const bool owner = warp != 2;  // arms the stage barrier with the tile's byte count
+    const int i_lo = warp == 2 ? 4 : 0, i_hi = warp == 0 ? 4 : 8;
     if (lane == 0) {
       if (kv == 0) tma_prefetch_desc(&tmQ);
       tma_prefetch_desc(kv ? &tmV : &tmK);
@@ -227,7 +230,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const Item x = prefill_item(p, total_qb, it);
       const int32_t* bt = p.block_table + (int64_t)x.b * p.bt_stride;
       const int nsb_valid = (x.kv_end + 15) / 16;  // sub-blocks holding visible keys
-      if (kv == 0 && lane == 0) {
+      if (warp == 0 && lane == 0) {
         mbar_wait(&bar.q_empty, (ic & 1u) ^ 1u);
         mbar_arrive_expect_tx(&bar.q_full, 2 * kTile);
         for (int h = 0; h < 2; ++h) {
@@ -247,17 +250,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint8_t* base = smem + (kv ? kOffV : kOffK) + s * kTile;
         if (lane == 0) {
           mbar_wait(emptyb, ph ^ 1u);
-          mbar_arrive_expect_tx(fullb, kTile);
+          if (owner) mbar_arrive_expect_tx(fullb, kTile);
         }
-        for (int i = 0; i < nbt; ++i) {
+        for (int i = i_lo; i < i_hi; ++i) {
           const int blk = __shfl_sync(0xffffffffu, id_cur, i);
           const int slot0 = ((jt * nbt + i) % n16) * 16;
           const int c1 = p.kv_tok_inner ? slot0 : x.kvh, c2 = p.kv_tok_inner ? x.kvh : slot0;
           if (lane == 0) {
             uint8_t* dst = base + i * 16 * 128;
-            if (i == 0) PATTN_K1_TRACE(20 + kv);
+            if (i == i_lo && owner) PATTN_K1_TRACE(20 + kv);
+#ifdef PATTN_NO_L2HINT
+            tma_load_4d(dst, tm, fullb, 0, c1, c2, blk);
+            tma_load_4d(dst + kHalf, tm, fullb, 64, c1, c2, blk);
+#else
             tma_load_4d_hint(dst, tm, fullb, 0, c1, c2, blk, pol_kv);
             tma_load_4d_hint(dst + kHalf, tm, fullb, 64, c1, c2, blk, pol_kv);
+#endif
           }
         }
         ++cnt;
@@ -340,8 +348,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (do_pv) ++vc;
       }
     }
-  } else if (warp < 4) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");  // warp 2 (TMEM allocator) idles
   } else {
     // ================================================================ softmax / correction / epilogue
     asm volatile("setmaxnreg.inc.sync.aligned.u32 224;\n" ::: "memory");
