@@ -75,7 +75,7 @@ constexpr int kHalfM = 128;    // rows per half (one UMMA M)
 constexpr int kM = 2 * kHalfM; // BLOCK_M
 constexpr int kN = 128;        // keys per KV tile
 constexpr int kD = 128;        // head dim
-constexpr int kThreads = 384;  // 12 warps
+constexpr int kThreads = 512;  // 16 warps
 constexpr uint32_t kTile = kN * kD * 2;  // 32 KB: one bf16 128x128 tile
 constexpr uint32_t kHalf = kTile / 2;    // 16 KB: one 64-wide d half
 constexpr int kKStages = 2;
@@ -202,18 +202,22 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int G = p.G;
   const int bq_half = p.block_q / 2;  // tokens per 128-row half
 
-  // register rebalancing per warpgroup: producer/MMA warpgroup 56, softmax warpgroups 224
-  // (128*56 + 256*224 = 64512 <= 65536)
+  // register rebalancing per warpgroup: warpgroup 0 (producers, MMA) 56, softmax warpgroups
+  // 1-2 208, warpgroup 3 (producer + spares) 40: 128*56 + 256*208 + 128*40 = 65536
 
-  if (warp == 0 || warp == 2 || warp == 3) {
+  if (warp == 0 || warp == 2 || warp == 3 || warp == 12) {
     // ================================================================ TMA producers
-    // warp 0: Q and sub-blocks 0-3 of every K tile, warp 2: K sub-blocks 4-7, warp 3: the V
-    // ring.  K and V rings are independent (a V stage still in use by PV never delays the
-    // next K tile the S MMA waits for) and the per-box TMA issue cost is spread over warps.
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
-    const int kv = warp == 3 ? 1 : 0;
-    const bool owner = warp != 2;  // arms the stage barrier with the tile's byte count
-    const int i_lo = warp == 2 ? 4 : 0, i_hi = warp == 0 ? 4 : 8;
+    // warp 0: Q and sub-blocks 0-3 of every K tile, warp 2: K sub-blocks 4-7, warp 3: V
+    // sub-blocks 0-3, warp 12: V sub-blocks 4-7.  K and V rings are independent (a V stage
+    // still in use by PV never delays the next K tile the S MMA waits for) and the per-box
+    // TMA issue cost (~150 clk) is spread over four warps.
+    if (warp < 4)
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
+    else
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
+    const int kv = (warp == 3 || warp == 12) ? 1 : 0;
+    const bool owner = warp == 0 || warp == 3;  // arms the stage barrier with the tile's byte count
+    const int i_lo = owner ? 0 : 4, i_hi = owner ? 4 : 8;
     if (lane == 0) {
       if (kv == 0) tma_prefetch_desc(&tmQ);
       tma_prefetch_desc(kv ? &tmV : &tmK);
@@ -348,9 +352,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (do_pv) ++vc;
       }
     }
+  } else if (warp >= 13) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");  // spare warps of warpgroup 3
   } else {
     // ================================================================ softmax / correction / epilogue
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;\n" ::: "memory");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 208;\n" ::: "memory");
     const int h = (warp - 4) >> 2;             // half a (0) or b (1)
     const int r = threadIdx.x - 128 - h * 128;  // row within the half == TMEM lane
     const uint32_t lane_off = (uint32_t)(32 * (warp & 3)) << 16;
