@@ -298,3 +298,27 @@ PATTN_DEVICE bool elect_one() {
   return pred != 0;
 }
 }  // namespace pattn
+
+namespace pattn {
+// packed fp32x2 (sm_100 FFMA2 / FADD2 / FMUL2): two fp32 lanes in one 64-bit register pair
+PATTN_DEVICE uint64_t f32x2(float lo, float hi) {
+  return (uint64_t)__float_as_uint(lo) | ((uint64_t)__float_as_uint(hi) << 32);
+}
+PATTN_DEVICE float f32x2_lo(uint64_t v) { return __uint_as_float((uint32_t)v); }
+PATTN_DEVICE float f32x2_hi(uint64_t v) { return __uint_as_float((uint32_t)(v >> 32)); }
+PATTN_DEVICE uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;\n" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+PATTN_DEVICE uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;\n" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+PATTN_DEVICE uint64_t fmul2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;\n" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+}  // namespace pattn

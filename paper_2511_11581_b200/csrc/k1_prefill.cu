@@ -411,22 +411,22 @@ __global__ void __launch_bounds__(kThreads, 1)
           m_use = m_new;
         }
         const float nbase = m_use == -INFINITY ? 0.f : -m_use;
-        float rsv[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) rsv[i] = 0.f;
+        // packed fp32x2 FMA-pipe ops (FFMA2 / FADD2, sm_100): half the instructions for the
+        // exponent argument and the row sum
+        const uint64_t ca2 = f32x2(ca, ca), nb2 = f32x2(nbase, nbase);
+        uint64_t rs2[4] = {0ull, 0ull, 0ull, 0ull};
         uint32_t pk[kN / 2];
 #pragma unroll
         for (int c = 0; c < kN; c += 2) {
-          // e^{scale*qk - m} in the log2 domain; pairs with (c & kPolyMask) == kPolyMask on the FMA pipe
-          const float x0 = fmaf(s[c], ca, nbase), x1 = fmaf(s[c + 1], ca, nbase);
-          const bool poly = ((c >> 1) & kPolyMask) == kPolyMask;
-          const float e0 = poly ? exp2_poly(x0) : fast_exp2(x0);
-          const float e1 = poly ? exp2_poly(x1) : fast_exp2(x1);
-          rsv[c & 7] += e0;
-          rsv[(c + 1) & 7] += e1;
+          // e^{scale*qk - m} in the log2 domain
+          const uint64_t xx = ffma2(f32x2(s[c], s[c + 1]), ca2, nb2);
+          const float e0 = fast_exp2(f32x2_lo(xx)), e1 = fast_exp2(f32x2_hi(xx));
+          const uint64_t ee = f32x2(e0, e1);
+          rs2[(c >> 1) & 3] = fadd2(rs2[(c >> 1) & 3], ee);
           pk[c >> 1] = pack_bf16(e0, e1);
         }
-        const float rs = ((rsv[0] + rsv[1]) + (rsv[2] + rsv[3])) + ((rsv[4] + rsv[5]) + (rsv[6] + rsv[7]));
+        const uint64_t r01 = fadd2(rs2[0], rs2[1]), r23 = fadd2(rs2[2], rs2[3]), rr = fadd2(r01, r23);
+        const float rs = f32x2_lo(rr) + f32x2_hi(rr);
         // O_h: PV_h(jt-1) was issued before S_h(jt) (in-order), so it is complete; the barrier
         // wait orders its TMEM writes before our correction.
         if (jt > 0) {
