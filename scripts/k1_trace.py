@@ -38,7 +38,7 @@ ev = ev[np.argsort(ev[:, 0], kind="stable")]
 ev = ev[ev[:, 0] > 0]
 t0 = ev[0, 0]
 names = {1: "K_ready", 2: "V_ready", 3: "Pa_ready", 4: "Pb_ready", 5: "PVa_issued", 6: "PVb_issued", 7: "Sa_issued",
-         8: "Sb_issued", 10: "SMa_start", 11: "SMb_start", 12: "SMa_done", 13: "SMb_done", 20: "K_load", 21: "V_load", 22: "K_issued", 23: "V_issued"}
+         8: "Sb_issued", 10: "SMa_start", 11: "SMb_start", 12: "SMa_done", 13: "SMb_done", 20: "K_load", 21: "V_load", 22: "K_issued", 23: "V_issued", 30: "SMa_ldS", 31: "SMb_ldS", 32: "SMa_max", 33: "SMb_max", 34: "SMa_exp", 35: "SMb_exp"}
 print("events", n)
 for t, c in ev[:160]:
     print(f"{int(t - t0):8d}  {names.get(int(c), c)}")
@@ -72,3 +72,9 @@ kr = ev[ev[:, 1] == 1, 0].astype(np.int64)
 # K tile j issued (ka[j]) -> MMA observed K ready (kr[j])
 m = min(len(ka), len(kr))
 print("K issued->ready median", np.median(kr[:m] - ka[:m]))
+
+def dur(a, b):
+    ta = ev[ev[:, 1] == a, 0].astype(np.int64); tb = ev[ev[:, 1] == b, 0].astype(np.int64)
+    m = min(len(ta), len(tb))
+    return np.median(tb[:m] - ta[:m]) if m else float("nan")
+print("softmax a phases: start->ldS", dur(10, 30), " ldS->max", dur(30, 32), " max->exp", dur(32, 34), " exp->done", dur(34, 12))

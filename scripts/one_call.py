@@ -16,10 +16,13 @@ from workloads.gen import generate_device  # noqa: E402
 name = sys.argv[1] if len(sys.argv) > 1 else "c2_decode8b"
 rep = int(sys.argv[2]) if len(sys.argv) > 2 else 1
 w = CONFIGS[name]
-if len(sys.argv) > 3:  # e.g. "16x4096:1" -> 16 sequences of (ctx 4096, q 1)
-    n, rest = sys.argv[3].split("x")
-    ctx, q = rest.split(":")
-    w = w.with_seqs([(int(ctx), int(q))] * int(n), name=name + "_small")
+if len(sys.argv) > 3:  # e.g. "16x4096:1+2x0:300" -> 16 x (ctx 4096, q 1) and 2 x (ctx 0, q 300)
+    seqs = []
+    for grp in sys.argv[3].split("+"):
+        n, rest = grp.split("x")
+        ctx, q = rest.split(":")
+        seqs += [(int(ctx), int(q))] * int(n)
+    w = w.with_seqs(seqs, name=name + "_small")
 inp = generate_device(w, seed=1, device="cuda")
 out = torch.empty_like(inp["q"])
 for _ in range(rep):
