@@ -52,7 +52,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--streams", type=int, default=1, help="1: serial; 2: decode kernels on a second stream")
+    ap.add_argument("--streams", type=int, default=2,
+                    help="2 (default): decode kernels on a second stream, concurrent with prefill; 1: serial")
     ap.add_argument("--flags", type=int, default=0)
     ap.add_argument("--seed", type=int, default=3003)
     return ap.parse_args()
@@ -310,6 +311,46 @@ def main():
         if kmask & (1 << k):
             kern_ms[pattn.KERNEL_NAMES[k]] = sum(kev[i][2 * k].elapsed_time(kev[i][2 * k + 1]) for i in range(K)) / K
 
+    # ---------------- the same step captured once as a CUDA graph and replayed (static grids,
+    # device-resident metadata: P:190-199); reported beside the eager number
+    graph = None
+    try:
+        gs = torch.cuda.Stream(dev)
+        gs2 = torch.cuda.Stream(dev) if args.streams == 2 else None
+        with torch.cuda.stream(gs):
+            pattn.unified_attention(q, kc, vc, bt, cu, sl, w.scale, w.num_kv_heads, w.block_size, out,
+                                    max_query_len=max_q, max_seq_len=max_L, flags=args.flags, stream=gs,
+                                    stream2=gs2)
+        torch.cuda.synchronize()
+        cg = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(cg, stream=gs):
+            pattn.unified_attention(q, kc, vc, bt, cu, sl, w.scale, w.num_kv_heads, w.block_size, out,
+                                    max_query_len=max_q, max_seq_len=max_L, flags=args.flags, stream=gs,
+                                    stream2=gs2)
+        for _ in range(3):
+            cg.replay()
+        torch.cuda.synchronize()
+        barrier()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        rs = torch.cuda.current_stream(dev)  # CUDAGraph.replay() launches on the current stream
+        g0.record(rs)
+        for _ in range(K):
+            cg.replay()
+        g1.record(rs)
+        torch.cuda.synchronize()
+        gms = torch.tensor([g0.elapsed_time(g1) / K], device=dev)
+        if world > 1:
+            dist.all_reduce(gms, op=dist.ReduceOp.MAX)
+        ref_out = out.clone()
+        out.fill_(0)
+        cg.replay()
+        torch.cuda.synchronize()
+        same = bool(torch.equal(out, ref_out))
+        graph = {"ms_per_step": float(gms.item()), "value": w.num_tokens * world / (float(gms.item()) * 1e-3),
+                 "replay_matches_eager": same}
+    except Exception as ex:  # reported, never fatal
+        graph = {"error": str(ex)[:200]}
+
     ms_t = torch.tensor([ms], device=dev)
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
@@ -414,6 +455,7 @@ def main():
         "kernel_ms": kern_ms,
         "clocks": sampler.summary(),
         "e2e": e2e,
+        "cuda_graph": graph,
         "gpu_launches": launches_per_step * K,
         "cpu_baseline": cpu,
         "algorithmic": {"prefill_tflop_per_step": work["prefill_flops"] / 1e12,
