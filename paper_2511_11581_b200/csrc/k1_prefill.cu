@@ -10,7 +10,10 @@
 // §4.1 runs between the two contractions.
 //
 // One CTA per SM, persistent over (Q block, KV head) work items (static launch grid,
-// P:401-406), longest (last) Q blocks first.  Warp roles (384 threads):
+// P:401-406), longest (last) Q blocks first.  Items are claimed dynamically: warp 0 takes
+// the next item index from a global atomic counter (reset by K5) and publishes it to the
+// CTA's other role warps through an 8-deep shared-memory ring, so a CTA that shares its SM
+// with the decode kernel (two streams) or drew short items simply claims fewer items.  Warp roles (384 threads):
 //   warp 0       TMA producer: Q (both halves, 4 boxes) and the K / V tiles (2 boxes per
 //                16-key sub-block; sub-blocks past the visible range are requested at block
 //                index num_blocks, out of bounds, so TMA zero-fills them) into K and V rings.
@@ -31,6 +34,8 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include "trace.cuh"
+PATTN_CTA_TRACE_DEFINE(k1)
 #ifdef PATTN_TRACE
 // debug timeline of CTA 0: one array per recording thread (no atomics: fire-and-forget stores)
 // slot = (role, index): role 0 MMA thread, 1/2 softmax WG a/b thread 0, 3/4 K/V producer lane 0
@@ -91,7 +96,7 @@ constexpr uint32_t kOffQ = 0;  // half a: [0, 32K), half b: [32K, 64K)
 constexpr uint32_t kOffK = kOffQ + 2 * kTile;
 constexpr uint32_t kOffV = kOffK + kKStages * kTile;
 constexpr uint32_t kOffBar = kOffV + kVStages * kTile;
-constexpr uint32_t kSmemBytes = kOffBar + 256 + 1024;
+constexpr uint32_t kSmemBytes = kOffBar + 512 + 1024;
 static_assert(kSmemBytes <= 227 * 1024, "shared memory budget");
 
 // TMEM columns
@@ -103,9 +108,15 @@ struct Bars {
   uint64_t k_full[kKStages], k_empty[kKStages];
   uint64_t v_full[kVStages], v_empty[kVStages];
   uint64_t s_full[2], p_full[2], pv_done[2], o_empty[2];
+  // dynamic work queue: warp 0 lane 0 claims items with an atomic counter (longest first) and
+  // publishes them through this ring; the other 12 role warps consume it in order
+  uint64_t item_full[8], item_empty[8];
+  int item_ring[8];
   uint32_t tmem_base;
 };
-static_assert(sizeof(Bars) <= 256, "barrier block");
+static_assert(sizeof(Bars) <= 512, "barrier block");
+constexpr int kItemRing = 8;
+constexpr int kItemConsumers = 12;  // warps 1, 2, 3, 12 and the 8 softmax warps
 
 struct Item {
   int b, kvh, q0, qlen, L, ctx, tok0, ntok, kv_end, ntiles;
@@ -159,6 +170,28 @@ PATTN_DEVICE void tc_mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_des
       : "memory");
 }
 
+// Consumer side of the item ring (whole warp): the n-th item of this CTA.
+PATTN_DEVICE int next_item(Bars& bar, uint32_t n, int lane) {
+  const uint32_t slot = n % kItemRing;
+  mbar_wait(&bar.item_full[slot], (n / kItemRing) & 1u);
+  const int it = reinterpret_cast<volatile int*>(bar.item_ring)[slot];
+  __syncwarp();
+  if (lane == 0) mbar_arrive(&bar.item_empty[slot]);
+  return it;
+}
+// Producer side (warp 0, whole warp): claim the next item globally and publish it.
+PATTN_DEVICE int publish_item(Bars& bar, uint32_t n, int lane, int* counter) {
+  int it = 0;
+  if (lane == 0) {
+    const uint32_t slot = n % kItemRing;
+    mbar_wait(&bar.item_empty[slot], ((n / kItemRing) & 1u) ^ 1u);
+    it = atomicAdd(counter, 1);
+    reinterpret_cast<volatile int*>(bar.item_ring)[slot] = it;
+    mbar_arrive(&bar.item_full[slot]);
+  }
+  return __shfl_sync(0xffffffffu, it, 0);
+}
+
 __global__ void __launch_bounds__(kThreads, 1)
     k1_prefill(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                const __grid_constant__ CUtensorMap tmV, Params p) {
@@ -167,6 +200,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   Bars& bar = *reinterpret_cast<Bars*>(smem + kOffBar);
   const uint32_t sbase = smem_u32(smem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  PATTN_CTA_BEGIN(k1);
+  // two-stream SM partition (K5's choice): surplus CTAs leave their SM to the decode kernel
+  if (p.partition && (int)blockIdx.x >= p.hdr[kHdrPrefillCtas]) return;
 #ifdef PATTN_TRACE
   const int trace_role = warp == 1 ? 0 : warp == 0 ? 3 : warp == 3 ? 4 : warp == 4 ? 1 : 2;
   unsigned int trace_cnt = 0;
@@ -188,6 +224,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&bar.p_full[h], kHalfM);
       mbar_init(&bar.pv_done[h], 1);
       mbar_init(&bar.o_empty[h], kHalfM);
+    }
+    for (int i = 0; i < kItemRing; ++i) {
+      mbar_init(&bar.item_full[i], 1);
+      mbar_init(&bar.item_empty[i], kItemConsumers);
     }
     fence_barrier_init();
   }
@@ -230,7 +270,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const CUtensorMap* tm = kv ? &tmV : &tmK;
     const int nst = kv ? kVStages : kKStages;
     uint32_t ic = 0, cnt = 0;
-    for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++ic) {
+    for (;; ++ic) {
+      const int it = warp == 0 ? publish_item(bar, ic, lane, p.hdr + kHdrPrefillCounter) : next_item(bar, ic, lane);
+      if (it >= n_items) break;
       const Item x = prefill_item(p, total_qb, it);
       const int32_t* bt = p.block_table + (int64_t)x.b * p.bt_stride;
       const int nsb_valid = (x.kv_end + 15) / 16;  // sub-blocks holding visible keys
@@ -289,7 +331,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool leader = elect_one();
     uint32_t ic = 0, kc = 0, vc = 0;
     uint32_t pc[2] = {0u, 0u};
-    for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++ic) {
+    for (;; ++ic) {
+      const int it = next_item(bar, ic, lane);
+      if (it >= n_items) break;
       const Item x = prefill_item(p, total_qb, it);
       mbar_wait(&bar.q_full, ic & 1u);
       tc_fence_after();
@@ -366,7 +410,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     __nv_bfloat16* O = static_cast<__nv_bfloat16*>(p.out);
     const float cs = p.scale_log2;
     const float ca = fmaxf(fabsf(cs), 1e-30f);  // scale 0: -inf * 0 would be NaN; 1e-30 * s ~ 0
-    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+    uint32_t ic = 0;
+    for (;; ++ic) {
+      const int it = next_item(bar, ic, lane);
+      if (it >= n_items) break;
       const Item x = prefill_item(p, total_qb, it);
       const int tk = h * bq_half + r / G;  // token of this row within the Q block
       const bool row_valid = tk < x.ntok;
@@ -497,6 +544,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       mbar_arrive(&bar.o_empty[h]);
     }
+    if (threadIdx.x == 128) PATTN_CTA_END(k1, ic);
   }
 
   tc_fence_before();

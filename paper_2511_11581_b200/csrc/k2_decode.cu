@@ -27,15 +27,26 @@
 // Slots at positions >= L_b of the last sub-block may hold anything (NaN): scores are
 // masked by select and those V rows are zeroed in shared memory before use
 // (reading R13).
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
+#include "trace.cuh"
+
+PATTN_CTA_TRACE_DEFINE(k2)
+PATTN_EV_TRACE_DEFINE(k2)
 
 namespace pattn {
 namespace {
 
 constexpr int kSub = 16;  // keys per ring stage (one mma M tile)
+constexpr int kItemRing = 16;
+#ifndef PATTN_K2_NP
+#define PATTN_K2_NP 2
+#endif
+constexpr int kNP = PATTN_K2_NP;  // producer warps
+constexpr size_t kItemRingBytes = kItemRing * (2 * sizeof(uint64_t) + sizeof(int));
 
 template <int D>
 struct DecodeShape {
@@ -75,7 +86,7 @@ __device__ __forceinline__ Item decode_item(const Params& p, int it) {
 }
 
 template <int D, int NCW>
-__global__ void __launch_bounds__((NCW + 1) * 32, 1)
+__global__ void __launch_bounds__((NCW + kNP) * 32, 1)
     k2_decode(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, Params p,
               int nst) {
   using S = DecodeShape<D>;
@@ -86,12 +97,22 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
   uint64_t* empty = full + nst;
   float* scratch = reinterpret_cast<float*>(empty + nst);  // [NCW][16 + 8*D]
   constexpr int kScr = 16 + 8 * D;
+  // dynamic work queue: the producer claims items from a global counter (reset by K5) and
+  // publishes them to the consumer warps through a kItemRing-deep ring
+  uint64_t* item_full = reinterpret_cast<uint64_t*>(scratch + NCW * kScr);
+  uint64_t* item_empty = item_full + kItemRing;
+  volatile int* item_ring = reinterpret_cast<volatile int*>(item_empty + kItemRing);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  PATTN_CTA_BEGIN(k2);
   if (threadIdx.x == 0) {
     for (int s = 0; s < nst; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
+    }
+    for (int i = 0; i < kItemRing; ++i) {
+      mbar_init(&item_full[i], 1);
+      mbar_init(&item_empty[i], NCW + kNP - 1);
     }
     fence_barrier_init();
   }
@@ -100,38 +121,65 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
   const int n_items = p.hdr[kHdrTotalChunks] * p.Hkv * p.HG;
   const int n16 = p.bs / kSub;
 
-  if (warp == 0) {
-    // ------------------------------------------------------------ producer
+  if (warp == 0 || warp > NCW) {
+    // ------------------------------------------------------------ producers
+    // kNP producer warps (warp 0 and warp NCW+1): sub-block g of the CTA is issued by
+    // producer g % kNP (the issue of a TMA box costs the issuing thread a few hundred
+    // cycles, so one thread alone caps a CTA at ~14 B/clk).  Producer 0 claims the items.
+    const int pw = warp == 0 ? 0 : warp - NCW;
     if (lane == 0) {
       tma_prefetch_desc(&tmK);
       tma_prefetch_desc(&tmV);
     }
     const uint64_t policy = l2_policy_evict_first();  // K/V are streamed exactly once
-    uint32_t g = 0;
-    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+    uint32_t g = 0;  // CTA-global sub-block counter; a multiple of NCW (and kNP) at item start
+    for (uint32_t ni = 0;; ++ni) {
+      int it = 0;
+      if (lane == 0) {
+        const uint32_t slot = ni % kItemRing;
+        if (pw == 0) {
+          mbar_wait(&item_empty[slot], ((ni / kItemRing) & 1u) ^ 1u);
+          it = atomicAdd(p.hdr + kHdrDecodeCounter, 1);
+          item_ring[slot] = it;
+          mbar_arrive(&item_full[slot]);
+        } else {
+          mbar_wait(&item_full[slot], (ni / kItemRing) & 1u);
+          it = item_ring[slot];
+          mbar_arrive(&item_empty[slot]);
+        }
+      }
+      it = __shfl_sync(0xffffffffu, it, 0);
+      if (it >= n_items) break;
       const Item x = decode_item(p, it);
       const int32_t* bt = p.block_table + (int64_t)x.b * p.bt_stride;
       for (int j0 = x.sb0; j0 < x.sb1; j0 += 32) {
         const int n = min(32, x.sb1 - j0);
         const int id = lane < n ? __ldg(bt + (j0 + lane) / n16) : 0;
-        for (int jj = 0; jj < n; ++jj) {
+        for (int jj = pw; jj < n; jj += kNP) {
           const int blk = __shfl_sync(0xffffffffu, id, jj);
           const int slot0 = ((j0 + jj) % n16) * kSub;
           if (lane == 0) {
-            const uint32_t s = g % nst;
-            const uint32_t ph = (g / nst) & 1u;
-            mbar_wait_tag(&empty[s], ph ^ 1u, 1000000 + (int)g, it, 0);
+            const uint32_t gg = g + (uint32_t)(j0 - x.sb0 + jj);
+            const uint32_t s = gg % nst;
+            mbar_wait_tag(&empty[s], ((gg / nst) & 1u) ^ 1u, 1000000 + (int)gg, it, 0);
+            PATTN_EV(k2, 0, gg);
             mbar_arrive_expect_tx(&full[s], S::kStageBytes);
             uint8_t* st = ring + (size_t)s * S::kStageBytes;
-            const int c1 = p.kv_tok_inner ? slot0 : x.kvh, c2 = p.kv_tok_inner ? x.kvh : slot0;
-#pragma unroll
-            for (int h = 0; h < S::kHalves; ++h)
-              tma_load_4d_hint(st + h * S::kHalfBytes, &tmK, &full[s], h * 64, c1, c2, blk, policy);
-#pragma unroll
-            for (int h = 0; h < S::kHalves; ++h)
-              tma_load_4d_hint(st + S::kOpBytes + h * S::kHalfBytes, &tmV, &full[s], h * 64, c1, c2, blk, policy);
+            // one box per operand: {64 d, 16 slots, D/64 d-halves} -> [half][slot][64 d]
+            tma_load_5d_hint(st, &tmK, &full[s], 0, slot0, 0, x.kvh, blk, policy);
+            tma_load_5d_hint(st + S::kOpBytes, &tmV, &full[s], 0, slot0, 0, x.kvh, blk, policy);
           }
-          ++g;
+        }
+      }
+      g += (uint32_t)(x.sb1 - x.sb0);
+      // pad to a multiple of NCW with empty stages, so that every item starts on consumer
+      // warp 0: sub-block j of an item always goes to warp j % NCW and the NCW-way merge
+      // is bitwise independent of which CTA (and after which items) runs the item
+      for (; g % NCW != 0; ++g) {
+        if (lane == 0 && (int)(g % kNP) == pw) {
+          const uint32_t s = g % nst;
+          mbar_wait(&empty[s], ((g / nst) & 1u) ^ 1u);
+          mbar_arrive(&full[s]);
         }
       }
     }
@@ -148,7 +196,15 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
   const uint32_t ring_u32 = smem_u32(ring);
   uint32_t g = 0;
 
-  for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+  uint32_t ni = 0;
+  for (;; ++ni) {
+    const uint32_t slot = ni % kItemRing;
+    mbar_wait(&item_full[slot], (ni / kItemRing) & 1u);
+    const int it = item_ring[slot];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&item_empty[slot]);
+    if (it >= n_items) break;
+    if (lane == 0 && cw == 0) PATTN_EV(k2, 4, ni);
     const Item x = decode_item(p, it);
     const int g_eff = min(8, p.G - x.hg * 8);
     const int head0 = x.kvh * p.G + x.hg * 8;
@@ -173,12 +229,14 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
     // Sub-block g (CTA-global counter) goes to consumer warp g % NCW, and nst is a multiple
     // of NCW, so every ring stage is always consumed by the same warp, in order.  (TMA loads
     // complete out of order: a waiter must have observed phase u-1 of a stage before it
-    // waits on phase u, otherwise the parity test aliases and returns early.)
-    const int j_first = (int)((cw + NCW - (g % NCW)) % NCW);
-    for (int j = j_first; j < nsb; j += NCW) {
+    // waits on phase u, otherwise the parity test aliases and returns early.)  Items start
+    // at g % NCW == 0 (the producer pads with empty stages), so warp cw takes j = cw mod NCW.
+    for (int j = cw; j < nsb; j += NCW) {
       const uint32_t gg = g + j;
       const uint32_t s = gg % nst;
+      if (lane == 0) PATTN_EV(k2, 1, gg);
       mbar_wait_tag(&full[s], (gg / nst) & 1u, (int)gg, it, j);
+      if (lane == 0) PATTN_EV(k2, 2, gg);
       const uint32_t kst = ring_u32 + s * S::kStageBytes;
       const uint32_t vst = kst + S::kOpBytes;
       const int valid = x.L - (x.sb0 + j) * kSub;  // slots [0, valid) hold real keys
@@ -246,8 +304,17 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
       __syncwarp();
       if (valid < kSub) fence_proxy_async_smem();  // generic zero-writes before the next TMA fill
       if (lane == 0) mbar_arrive(&empty[s]);
+      if (lane == 0) PATTN_EV(k2, 3, gg);
     }
     g += nsb;
+    for (; g % NCW != 0; ++g) {  // the producer's padding stages
+      if ((int)(g % NCW) == cw) {
+        const uint32_t s = g % nst;
+        mbar_wait(&full[s], (g / nst) & 1u);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+      }
+    }
 
     // ---- merge the NCW warp states of this item
 #pragma unroll
@@ -295,7 +362,9 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
       }
     }
     named_bar_sync(1, NCW * 32);
+    if (lane == 0 && cw == 0) PATTN_EV(k2, 5, ni);
   }
+  if (warp == 1 && lane == 0) PATTN_CTA_END(k2, ni);
 }
 
 template <int D, int NCW>
@@ -304,7 +373,7 @@ cudaError_t launch_dw(const Params& p, const DecodeLaunch& dl, const CUtensorMap
   auto kern = k2_decode<D, NCW>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dl.smem);
   if (e != cudaSuccess) return e;
-  kern<<<dl.grid, (NCW + 1) * 32, dl.smem, stream>>>(tmK, tmV, p, dl.stages);
+  kern<<<dl.grid, (NCW + kNP) * 32, dl.smem, stream>>>(tmK, tmV, p, dl.stages);
   return cudaGetLastError();
 }
 
@@ -328,15 +397,15 @@ int env_or(const char* name, int dflt) {
 DecodeLaunch plan_decode(const Params& p, int num_sms, size_t max_smem) {
   DecodeLaunch dl;
   dl.consumer_warps = env_or("PATTN_DECODE_WARPS", 4) == 8 ? 8 : 4;
-  int ctas = env_or("PATTN_DECODE_CTAS", 3);
+  int ctas = env_or("PATTN_DECODE_CTAS", 2);
   if (ctas < 1) ctas = 1;
   if (ctas > 4) ctas = 4;
   const size_t stage = (size_t)4 * kSub * p.D;  // K + V of one 16-key sub-block, bf16
   const size_t scratch = (size_t)dl.consumer_warps * (16 + 8 * p.D) * sizeof(float);
-  const size_t fixed = 1024 /*align slack*/ + scratch;
+  const size_t fixed = 1024 /*align slack*/ + scratch + kItemRingBytes;
   const size_t per_cta = (max_smem < 228 * 1024 ? max_smem : 228 * 1024) / ctas - 1024;
   const size_t budget = per_cta > fixed ? per_cta - fixed : 0;
-  size_t want = (size_t)env_or("PATTN_DECODE_RING_KB", 64) * 1024;
+  size_t want = (size_t)env_or("PATTN_DECODE_RING_KB", 96) * 1024;
   if (want > budget) want = budget;
   int st = (int)(want / (stage + 16));
   if (st > 64) st = 64;
@@ -345,7 +414,7 @@ DecodeLaunch plan_decode(const Params& p, int num_sms, size_t max_smem) {
   dl.stages = st;
   dl.smem = fixed + (size_t)st * (stage + 16);
   const long long max_items = (long long)p.max_chunks * p.Hkv * p.HG;
-  const long long g = (long long)num_sms * ctas;
+  const long long g = (long long)std::min(num_sms, std::max(1, env_or("PATTN_DECODE_SMS", num_sms))) * ctas;
   dl.grid = (int)(max_items < g ? max_items : g);
   if (dl.grid < 1) dl.grid = 1;
   return dl;

@@ -22,114 +22,168 @@ namespace pattn {
 
 namespace {
 
-constexpr int kThreads = 1024;
+constexpr int kMaxThreads = 1024;
 
-// Block-wide exclusive scan of one int per thread; returns the exclusive prefix and
-// writes the block total to *total.
-__device__ int block_exclusive_scan(int v, int* s_warp, int* total) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int x = v;
+// Block-wide sum of one unsigned 64-bit value per thread (all threads get the total).
+__device__ unsigned long long block_sum_u64(unsigned long long v, unsigned long long* s_red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (lane == 0) s_red[warp] = v;
+  __syncthreads();
+  unsigned long long t = lane < nw ? s_red[lane] : 0ull;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  __syncthreads();
+  return t;
+}
+
+// Block-wide exclusive scan of two ints per thread at once (x: Q blocks, y: decode
+// segments); returns the exclusive prefixes and writes the block totals.
+__device__ int2 block_exclusive_scan2(int2 v, int2* s_warp, int2* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int2 x = v;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    int y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
+    const int a = __shfl_up_sync(0xffffffffu, x.x, o), b = __shfl_up_sync(0xffffffffu, x.y, o);
+    if (lane >= o) {
+      x.x += a;
+      x.y += b;
+    }
   }
   if (lane == 31) s_warp[warp] = x;
   __syncthreads();
   if (warp == 0) {
-    int w = (lane < (kThreads >> 5)) ? s_warp[lane] : 0;
+    int2 w = lane < nw ? s_warp[lane] : make_int2(0, 0);
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      int y = __shfl_up_sync(0xffffffffu, w, o);
-      if (lane >= o) w += y;
+      const int a = __shfl_up_sync(0xffffffffu, w.x, o), b = __shfl_up_sync(0xffffffffu, w.y, o);
+      if (lane >= o) {
+        w.x += a;
+        w.y += b;
+      }
     }
     s_warp[lane] = w;  // inclusive over warps
   }
   __syncthreads();
-  int warp_excl = warp ? s_warp[warp - 1] : 0;
-  *total = s_warp[(kThreads >> 5) - 1];
+  const int2 we = warp ? s_warp[warp - 1] : make_int2(0, 0);
+  *total = s_warp[nw - 1];
   __syncthreads();
-  return warp_excl + x - v;
+  return make_int2(we.x + x.x - v.x, we.y + x.y - v.y);
 }
 
-__global__ void __launch_bounds__(kThreads) k5_metadata(Params p) {
-  __shared__ int s_warp[32];
-  __shared__ unsigned long long s_blocks;
-  __shared__ int s_ndec;
+// One CTA of min(1024, roundup(B, 32)) threads; sequence b is handled by thread b % blockDim
+// (one pass over the batch when B <= blockDim: per-sequence values stay in registers).
+__global__ void __launch_bounds__(kMaxThreads) k5_metadata(Params p) {
+  __shared__ unsigned long long s_red[32];
+  __shared__ int2 s_scan[32];
   const int B = p.B;
-  if (threadIdx.x == 0) {
-    s_blocks = 0ull;
-    s_ndec = 0;
-  }
-  __syncthreads();
+  const int nt = blockDim.x;
+  const bool one_pass = B <= nt;
 
-  // pass 1: decode count and total decode KV blocks
-  unsigned long long my_blocks = 0;
-  int my_dec = 0;
-  for (int b = threadIdx.x; b < B; b += kThreads) {
-    int qb = p.cu_seqlens_q[b + 1] - p.cu_seqlens_q[b];
+  // pass 1: decode count and total decode KV blocks (+ the partition cost model's inputs:
+  // K1 (Q block, 128-key tile) pairs and decode keys)
+  int q0 = 0, L0 = 0;  // this thread's sequence when one_pass
+  unsigned long long my_blocks = 0, my_tiles = 0, my_keys = 0, my_dec = 0;
+  for (int b = threadIdx.x; b < B; b += nt) {
+    const int qb = __ldg(p.cu_seqlens_q + b + 1) - __ldg(p.cu_seqlens_q + b);
+    const int L = __ldg(p.seq_lens + b);
+    q0 = qb;
+    L0 = L;
     if (p.decode_to_k2 && qb == 1) {
       my_dec += 1;
-      my_blocks += (unsigned long long)((p.seq_lens[b] + p.bs - 1) / p.bs);
+      my_blocks += (unsigned long long)((L + p.bs - 1) / p.bs);
+      my_keys += (unsigned long long)L;
+    } else if (p.partition && qb > 0) {
+      const int ctx = L - qb;
+      for (int t0 = 0; t0 < qb; t0 += p.block_q)
+        my_tiles += (unsigned long long)((ctx + min(t0 + p.block_q, qb) + 127) / 128);
     }
   }
-  if (my_dec) {
-    atomicAdd(&s_ndec, my_dec);
-    atomicAdd(&s_blocks, my_blocks);
+  const unsigned long long n_dec = block_sum_u64(my_dec, s_red);
+  const unsigned long long dec_blocks = block_sum_u64(my_blocks, s_red);
+  unsigned long long tiles = 0, keys = 0;
+  if (p.partition) {
+    tiles = block_sum_u64(my_tiles, s_red);
+    keys = block_sum_u64(my_keys, s_red);
   }
-  __syncthreads();
 
   const long long units = (long long)p.Hkv * p.HG;
   long long C;
   if (p.split_mode == 1) {
     C = INT_MAX;
   } else {
-    long long want = ((long long)s_blocks * units + p.target_items - 1) / p.target_items;
+    long long want = ((long long)dec_blocks * units + p.target_items - 1) / p.target_items;
     C = want > p.min_chunk_blocks ? want : p.min_chunk_blocks;
     if (C < 1) C = 1;
   }
 
-  // pass 2: scans
+  // pass 2: scans of Q blocks (cu_q_blocks) and decode segments (cu_chunks)
   int carry_qb = 0, carry_ch = 0;
-  for (int base = 0; base < B; base += kThreads) {
-    int b = base + threadIdx.x;
-    int nqb = 0, nch = 0;
+  for (int base = 0; base < B; base += nt) {
+    const int b = base + threadIdx.x;
+    int2 cnt = make_int2(0, 0);
     if (b < B) {
-      int qb = p.cu_seqlens_q[b + 1] - p.cu_seqlens_q[b];
+      int qb = q0, L = L0;
+      if (!one_pass) {
+        qb = __ldg(p.cu_seqlens_q + b + 1) - __ldg(p.cu_seqlens_q + b);
+        L = __ldg(p.seq_lens + b);
+      }
       if (p.decode_to_k2 && qb == 1) {
-        long long nblk = (p.seq_lens[b] + p.bs - 1) / p.bs;
-        nch = (int)((nblk + C - 1) / C);
+        const long long nblk = (L + p.bs - 1) / p.bs;
+        cnt.y = (int)((nblk + C - 1) / C);
       } else if (qb > 0) {
-        nqb = (qb + p.block_q - 1) / p.block_q;
+        cnt.x = (qb + p.block_q - 1) / p.block_q;
       }
     }
-    int tot_qb, tot_ch;
-    int ex_qb = block_exclusive_scan(nqb, s_warp, &tot_qb);
-    int ex_ch = block_exclusive_scan(nch, s_warp, &tot_ch);
+    int2 tot;
+    const int2 ex = block_exclusive_scan2(cnt, s_scan, &tot);
     if (b < B) {
-      p.cu_qb[b] = carry_qb + ex_qb;
-      p.cu_ch[b] = carry_ch + ex_ch;
+      p.cu_qb[b] = carry_qb + ex.x;
+      p.cu_ch[b] = carry_ch + ex.y;
     }
-    carry_qb += tot_qb;
-    carry_ch += tot_ch;
+    carry_qb += tot.x;
+    carry_ch += tot.y;
   }
   if (threadIdx.x == 0) {
     p.cu_qb[B] = carry_qb;
     p.cu_ch[B] = carry_ch;
     p.hdr[kHdrTotalQBlocks] = carry_qb;
-    p.hdr[kHdrNumDecodes] = s_ndec;
+    p.hdr[kHdrNumDecodes] = (int)n_dec;
     p.hdr[kHdrTotalChunks] = carry_ch;
     p.hdr[kHdrBlockQ] = p.block_q;
     p.hdr[kHdrChunkBlocks] = (int)(C > INT_MAX ? INT_MAX : C);
     p.hdr[kHdrPrefillCounter] = 0;
     p.hdr[kHdrDecodeCounter] = 0;
+    // SM partition for concurrent K1 / K2: P minimising max(prefill time on P SMs, decode
+    // time on the other SMs, capped by HBM), from per-SM rates of the two kernels.
+    int P = p.num_sms;
+    if (p.partition) {
+      if (p.prefill_ctas_fixed > 0) {
+        P = min(p.prefill_ctas_fixed, p.num_sms);
+      } else if (tiles > 0 && keys > 0) {
+        // prefill time tp / c on c SMs; decode time bytes / min((S - c) b, HBM).  Balance
+        // point c* = S tp b / (tp b + bytes); below c_hbm = S - HBM / b the decode side is
+        // HBM-bound anyway, so P = max(c*, c_hbm).
+        const float S = (float)p.num_sms;
+        const float tp = (float)tiles * (float)p.Hkv * p.k1_tile_us * 1e-6f;  // SM-s
+        const float bytes = (float)keys * (float)p.Hkv * (float)p.D * 4.0f;   // K + V bf16
+        const float b = p.k2_sm_gbs * 1e9f;                                   // B/s per SM
+        const float cstar = S * tp * b / (tp * b + bytes);
+        const float chbm = S - p.hbm_gbs / p.k2_sm_gbs;
+        P = (int)(fmaxf(cstar, chbm) + 0.5f);
+        P = max(1, min(P, p.num_sms - 1));
+      }
+    }
+    p.hdr[kHdrPrefillCtas] = P;
   }
 }
 
 }  // namespace
 
 cudaError_t launch_metadata(const Params& p, cudaStream_t stream) {
-  k5_metadata<<<1, kThreads, 0, stream>>>(p);
+  const int threads = p.B >= kMaxThreads ? kMaxThreads : ((p.B + 31) / 32) * 32;
+  k5_metadata<<<1, threads < 32 ? 32 : threads, 0, stream>>>(p);
   return cudaGetLastError();
 }
 

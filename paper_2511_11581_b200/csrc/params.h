@@ -15,6 +15,7 @@ enum HdrWord {
   kHdrChunkBlocks = 4,   // decode segment length cap, in KV blocks
   kHdrPrefillCounter = 5,  // dynamic work counters (reset by K5)
   kHdrDecodeCounter = 6,
+  kHdrPrefillCtas = 7,   // two-stream SM partition: K1 CTAs that work (the rest exit at once)
   kHdrWords = 64
 };
 
@@ -39,6 +40,14 @@ struct Params {
   int32_t min_chunk_blocks;
   int32_t num_sms;
   int32_t kv_tok_inner;   // TMA dim order: 1 -> (d, slot, kvh, blk) [HND], 0 -> (d, kvh, slot, blk) [NHD]
+  // Two-stream SM partition (K1 and K2 concurrent): K5 picks the number of SMs P for the
+  // prefill kernel from the batch (cost model below); K1 CTAs >= P exit at once so that the
+  // decode kernel's CTAs take those SMs.  partition 0: off (serial or single kernel).
+  int32_t partition;
+  int32_t prefill_ctas_fixed;  // > 0: use this P instead of the model (sweeps)
+  float k1_tile_us;            // K1 cost per (128-key tile x 256-row Q block) on one SM
+  float k2_sm_gbs;             // K2 K/V streaming rate of one SM (2 CTAs), GB/s
+  float hbm_gbs;               // K2 ceiling: HBM read bandwidth, GB/s
   // strides (elements)
   int64_t q_st_tok, q_st_head;
   int64_t kv_st_blk, kv_st_tok, kv_st_head;

@@ -63,6 +63,11 @@ int env_int(const char* name, int dflt) {
   return (v && *v) ? atoi(v) : dflt;
 }
 
+float env_float(const char* name, float dflt) {
+  const char* v = getenv(name);
+  return (v && *v) ? (float)atof(v) : dflt;
+}
+
 thread_local char g_last_error[256] = "";
 
 pattn_status_t cuda_fail(cudaError_t e) {
@@ -253,6 +258,26 @@ bool encode_kv_map(CUtensorMap* tm, const pattn_problem_t* p, const void* base, 
   return r == CUDA_SUCCESS;
 }
 
+// H2b: 5-D view {64 d, slot, D/64 d-halves, head, block} (strides deliberately not nested:
+// the d-half dim, 128 B, sits outside the slot dim) so that ONE box {64, 16, D/64, 1, 1}
+// brings a whole 16-key sub-block of one head into shared memory as [half][slot][64 d],
+// the layout two 4-D boxes give -- half the TMA issues for the decode producer.
+bool encode_kv_map5(CUtensorMap* tm, const pattn_problem_t* p, const void* base) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  const int halves = p->head_dim / 64;
+  cuuint64_t dims[5] = {64, (cuuint64_t)p->block_size, (cuuint64_t)halves, (cuuint64_t)p->num_kv_heads,
+                        (cuuint64_t)p->num_blocks};
+  cuuint64_t strides[4] = {(cuuint64_t)p->kv_stride_tok * 2, 128, (cuuint64_t)p->kv_stride_head * 2,
+                           (cuuint64_t)p->kv_stride_blk * 2};
+  cuuint32_t box[5] = {64, 16, (cuuint32_t)halves, 1, 1};
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 // Q viewed as [T][Hkv][G][D]: box {64 d, G heads, BLOCK_Q tokens} -> BLOCK_M = BLOCK_Q*G rows
 // of 128 B, token-major / head-minor (reading R8).
 bool encode_q_map(CUtensorMap* tm, const pattn_problem_t* p, const void* q, int block_q) {
@@ -313,15 +338,29 @@ pattn_status_t run(const pattn_problem_t* p, const void* q, const void* k_cache,
   k.part_l = reinterpret_cast<float*>(ws + pl.off_pl);
   k.part_acc = reinterpret_cast<float*>(ws + pl.off_pacc);
 
-  CUtensorMap tmK, tmV, tmQ;
+  CUtensorMap tmK, tmV, tmQ, tmK5, tmV5;
   if (!metadata_only) {
-    if (pl.use_k2 || pl.use_k1) {
+    if (pl.use_k2) {
+      if (!encode_kv_map5(&tmK5, p, k_cache) || !encode_kv_map5(&tmV5, p, v_cache)) return PATTN_ERR_UNSUPPORTED;
+    }
+    if (pl.use_k1) {
       if (!encode_kv_map(&tmK, p, k_cache, pl.kv_tok_inner) || !encode_kv_map(&tmV, p, v_cache, pl.kv_tok_inner))
         return PATTN_ERR_UNSUPPORTED;
     }
     if (pl.use_k1) {
       if (!encode_q_map(&tmQ, p, q, pl.block_q)) return PATTN_ERR_UNSUPPORTED;
     }
+  }
+
+  const bool two = !metadata_only && (s2 != s1) && pl.use_k2 && (pl.use_k1 || pl.use_k4);
+  if (two && pl.use_k1) {
+    // K1 and K2 run concurrently on disjoint SMs; K5 sizes the split from the batch with a
+    // per-SM cost model of the two kernels (measured on B200)
+    k.partition = 1;
+    k.prefill_ctas_fixed = env_int("PATTN_PREFILL_SMS", 0);
+    k.k1_tile_us = env_float("PATTN_K1_TILE_US", 2.8f);
+    k.k2_sm_gbs = env_float("PATTN_K2_SM_GBS", 61.f);
+    k.hbm_gbs = env_float("PATTN_HBM_GBS", 6300.f);
   }
 
   EventRec ev{opts};
@@ -333,7 +372,6 @@ pattn_status_t run(const pattn_problem_t* p, const void* q, const void* k_cache,
   if (metadata_only) return PATTN_OK;
 
   cudaEvent_t fork = nullptr, join = nullptr;
-  const bool two = (s2 != s1) && pl.use_k2 && (pl.use_k1 || pl.use_k4);
   if (two) {
     cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&join, cudaEventDisableTiming);
@@ -341,20 +379,24 @@ pattn_status_t run(const pattn_problem_t* p, const void* q, const void* k_cache,
     cudaStreamWaitEvent(s2, fork, 0);
   }
   cudaStream_t sd = two ? s2 : s1;
+  // Two streams: the prefill kernel is issued first so that its (one-per-SM) CTAs take
+  // their SMs before the decode grid spreads over the GPU; the CTAs beyond K5's partition
+  // exit at once, the decode CTAs fill those SMs and, claiming items dynamically, the SMs
+  // the prefill CTAs release when they finish.
+  if (pl.use_k1) {
+    ev.rec(2 * PATTN_KERNEL_PREFILL, s1);
+    e = launch_prefill(k, pl.pl, tmQ, tmK, tmV, s1);
+    ev.rec(2 * PATTN_KERNEL_PREFILL + 1, s1);
+    if (e != cudaSuccess) return cuda_fail(e);
+  }
   if (pl.use_k2) {
     ev.rec(2 * PATTN_KERNEL_DECODE, sd);
-    e = launch_decode(k, pl.dl, tmK, tmV, sd);
+    e = launch_decode(k, pl.dl, tmK5, tmV5, sd);
     ev.rec(2 * PATTN_KERNEL_DECODE + 1, sd);
     if (e != cudaSuccess) return cuda_fail(e);
     ev.rec(2 * PATTN_KERNEL_REDUCE, sd);
     e = launch_reduce(k, sd);
     ev.rec(2 * PATTN_KERNEL_REDUCE + 1, sd);
-    if (e != cudaSuccess) return cuda_fail(e);
-  }
-  if (pl.use_k1) {
-    ev.rec(2 * PATTN_KERNEL_PREFILL, s1);
-    e = launch_prefill(k, pl.pl, tmQ, tmK, tmV, s1);
-    ev.rec(2 * PATTN_KERNEL_PREFILL + 1, s1);
     if (e != cudaSuccess) return cuda_fail(e);
   }
   if (pl.use_k4) {

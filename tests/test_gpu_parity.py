@@ -209,6 +209,20 @@ def test_two_stream_equals_serial():
     assert torch.equal(a, b)
 
 
+def test_dynamic_scheduling_is_bitwise_deterministic():
+    """Work items are claimed from global counters, so the item -> CTA mapping changes from run to
+    run (and with two streams); every item's arithmetic must not depend on it."""
+    seqs = tuple([(3000 + 37 * i, 1) for i in range(96)] + [(200 * i, 300 + 50 * i) for i in range(6)])
+    w = Workload("dyn", seqs, 32, 8, 128, 16, "bf16")
+    batch = generate(w, seed=15, dist="peaked", poison=True)
+    db = DeviceBatch(batch)
+    a = db.run().clone()
+    s2 = torch.cuda.Stream()
+    for i in range(6):
+        b = db.run(stream2=s2) if i % 2 else db.run()
+        assert torch.equal(a, b), f"run {i}"
+
+
 def test_cuda_graph_capture_and_replay_with_new_metadata():
     """The call is sync-free with data-independent grids (static launch grid), so it can
     be captured once and replayed with different device-resident metadata."""
