@@ -78,13 +78,23 @@ namespace {
 
 constexpr int kHalfM = 128;    // rows per half (one UMMA M)
 constexpr int kM = 2 * kHalfM; // BLOCK_M
-constexpr int kN = 128;        // keys per KV tile
+constexpr int kN = 64;         // keys per KV tile
 constexpr int kD = 128;        // head dim
 constexpr int kThreads = 512;  // 16 warps
-constexpr uint32_t kTile = kN * kD * 2;  // 32 KB: one bf16 128x128 tile
-constexpr uint32_t kHalf = kTile / 2;    // 16 KB: one 64-wide d half
-constexpr int kKStages = 2;
-constexpr int kVStages = 3;  // V waits on PV (later than S), so it gets the deeper ring
+constexpr uint32_t kQTile = kHalfM * kD * 2;  // 32 KB: one 128-row half of the Q block
+constexpr uint32_t kHalf = kQTile / 2;         // 16 KB: one 64-wide d half of it
+constexpr uint32_t kTile = kN * kD * 2;        // 16 KB: one K or V tile (64 keys)
+constexpr uint32_t kSub16Bytes = 16 * kD * 2;  // 4 KB: one 16-key sub-block of K or V
+// K / V tile layout: sub-block i at i*4K = [8-slot group g][d half h][8 slots][64 d], i.e.
+// 8-key group G = 2i+g at G*2048 + h*1024 (SW128 atoms of 8 rows x 128 B)
+#ifndef PATTN_K1_KST
+#define PATTN_K1_KST 4
+#endif
+#ifndef PATTN_K1_VST
+#define PATTN_K1_VST 5
+#endif
+constexpr int kKStages = PATTN_K1_KST;
+constexpr int kVStages = PATTN_K1_VST;  // V waits on PV (later than S), so it gets the deeper ring
 constexpr float kRescaleThreshold = 8.0f;  // log2 domain: rescale O only if the max grows by > 2^8
 #ifndef PATTN_POLY_MASK
 #define PATTN_POLY_MASK 255  // measured: FMA-pipe exp2 did not pay off here
@@ -93,34 +103,41 @@ constexpr int kPolyMask = PATTN_POLY_MASK;  // exp2 pair j on the FMA pipe iff (
 
 // shared-memory map (offsets from a 1024-aligned base)
 constexpr uint32_t kOffQ = 0;  // half a: [0, 32K), half b: [32K, 64K)
-constexpr uint32_t kOffK = kOffQ + 2 * kTile;
+constexpr uint32_t kOffK = kOffQ + 2 * kQTile;
 constexpr uint32_t kOffV = kOffK + kKStages * kTile;
 constexpr uint32_t kOffBar = kOffV + kVStages * kTile;
 constexpr uint32_t kSmemBytes = kOffBar + 512 + 1024;
 static_assert(kSmemBytes <= 227 * 1024, "shared memory budget");
 
 // TMEM columns
-constexpr uint32_t kTmemS = 0;    // S_x at x*128 (P_x aliased on its first 64 columns)
+constexpr uint32_t kTmemS = 0;    // S buffer (half x, tile parity y) at x*128 + y*64 (P aliased on its first 32 cols)
 constexpr uint32_t kTmemO = 256;  // O_x at 256 + x*128
 
 struct Bars {
   uint64_t q_full, q_empty;
   uint64_t k_full[kKStages], k_empty[kKStages];
   uint64_t v_full[kVStages], v_empty[kVStages];
-  uint64_t s_full[2], p_full[2], pv_done[2], o_empty[2];
-  // dynamic work queue: warp 0 lane 0 claims items with an atomic counter (longest first) and
-  // publishes them through this ring; the other 12 role warps consume it in order
-  uint64_t item_full[8], item_empty[8];
-  int item_ring[8];
+  uint64_t s_full[2][2], p_full[2], pv_done[2], o_empty[2];
+  // dynamic work queue (see ItemSlot)
+  uint64_t item_full[2], item_empty[2];
   uint32_t tmem_base;
 };
-static_assert(sizeof(Bars) <= 512, "barrier block");
-constexpr int kItemRing = 8;
-constexpr int kItemConsumers = 12;  // warps 1, 2, 3, 12 and the 8 softmax warps
+constexpr int kItemRing = 2;
+constexpr int kItemConsumers = 13;  // warps 0-3, 12 and the 8 softmax warps
 
 struct Item {
   int b, kvh, q0, qlen, L, ctx, tok0, ntok, kv_end, ntiles;
 };
+// Scheduler warp 13 claims the next item from the global counter (longest first), decodes it
+// and fetches the block-table entries of its first KV tile while the CTA still works on the
+// current item, so that neither the claim's atomic nor the dependent metadata / block-table
+// loads sit on the critical path at item boundaries.  ntiles < 0 ends the stream.
+struct ItemSlot {
+  Item x;
+  int ids[8];  // paged block of each 16-key sub-block of KV tile 0 (num_blocks: past the end)
+};
+constexpr uint32_t kOffItems = sizeof(Bars);
+static_assert(sizeof(Bars) + kItemRing * sizeof(ItemSlot) <= 512, "barrier block");
 
 __device__ __forceinline__ Item prefill_item(const Params& p, int total_qb, int it) {
   Item x;
@@ -154,10 +171,27 @@ PATTN_DEVICE float exp2_poly(float x) {
   const float t = __fadd_rn(x, 12582912.f);      // 1.5 * 2^23: n = rint(x) in the low mantissa bits
   const float n = __fadd_rn(t, -12582912.f);
   const float f = __fadd_rn(x, -n);
-  float pp = fmaf(0.05517161265015602f, f, 0.24261116981506348f);
-  pp = fmaf(pp, f, 0.6932610273361206f);
-  pp = fmaf(pp, f, 0.9999280571937561f);
+  float pp = fmaf(0.05500858277082443f, f, 0.24221037328243256f);
+  pp = fmaf(pp, f, 0.6932829022407532f);
+  pp = fmaf(pp, f, 1.0f);
   return __int_as_float(__float_as_int(pp) + (__float_as_int(t) << 23));
+}
+
+// Packed form on the FMA pipe (FADD2/FFMA2) for a pair of exponents; x <= 0 or -inf.
+PATTN_DEVICE uint64_t exp2_poly2(uint64_t xx) {
+  const float x0 = fmaxf(f32x2_lo(xx), -127.f), x1 = fmaxf(f32x2_hi(xx), -127.f);
+  const uint64_t x = f32x2(x0, x1);
+  const uint64_t t = fadd2(x, f32x2(12582912.f, 12582912.f));  // n = rint(x) in the low mantissa bits
+  const uint64_t n = fadd2(t, f32x2(-12582912.f, -12582912.f));
+  const uint64_t f = fadd2(x, n ^ 0x8000000080000000ull);       // x - n in [-0.5, 0.5]
+  // p(f) = 1 + c1 f + c2 f^2 + c3 f^3, relative-minimax on [-0.5, 0.5] with p(0) = 1 exactly
+  // (so a lone maximum gets exactly P = 1, like ex2.approx), max relative error 1.0e-4
+  uint64_t pp = ffma2(f32x2(0.05500858277082443f, 0.05500858277082443f), f,
+                      f32x2(0.24221037328243256f, 0.24221037328243256f));
+  pp = ffma2(pp, f, f32x2(0.6932829022407532f, 0.6932829022407532f));
+  pp = ffma2(pp, f, f32x2(1.0f, 1.0f));
+  const uint32_t lo = (uint32_t)pp + ((uint32_t)t << 23), hi = (uint32_t)(pp >> 32) + ((uint32_t)(t >> 32) << 23);
+  return (uint64_t)lo | ((uint64_t)hi << 32);
 }
 
 // O[tmem] (+)= A[tmem] * B[smem desc]; kind::f16, A (P) K-major in TMEM.
@@ -170,34 +204,35 @@ PATTN_DEVICE void tc_mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_des
       : "memory");
 }
 
-// Consumer side of the item ring (whole warp): the n-th item of this CTA.
-PATTN_DEVICE int next_item(Bars& bar, uint32_t n, int lane) {
+// Consumer side of the item ring (whole warp): the n-th item of this CTA (and, for the
+// producers, the block ids of its first tile).
+PATTN_DEVICE Item next_item(Bars& bar, const ItemSlot* ring, uint32_t n, int lane, int* ids0 = nullptr) {
   const uint32_t slot = n % kItemRing;
   mbar_wait(&bar.item_full[slot], (n / kItemRing) & 1u);
-  const int it = reinterpret_cast<volatile int*>(bar.item_ring)[slot];
+  const volatile ItemSlot* e = ring + slot;
+  Item x;
+  x.b = e->x.b;
+  x.kvh = e->x.kvh;
+  x.q0 = e->x.q0;
+  x.qlen = e->x.qlen;
+  x.L = e->x.L;
+  x.ctx = e->x.ctx;
+  x.tok0 = e->x.tok0;
+  x.ntok = e->x.ntok;
+  x.kv_end = e->x.kv_end;
+  x.ntiles = e->x.ntiles;
+  if (ids0) *ids0 = e->ids[lane & 7];
   __syncwarp();
   if (lane == 0) mbar_arrive(&bar.item_empty[slot]);
-  return it;
-}
-// Producer side (warp 0, whole warp): claim the next item globally and publish it.
-PATTN_DEVICE int publish_item(Bars& bar, uint32_t n, int lane, int* counter) {
-  int it = 0;
-  if (lane == 0) {
-    const uint32_t slot = n % kItemRing;
-    mbar_wait(&bar.item_empty[slot], ((n / kItemRing) & 1u) ^ 1u);
-    it = atomicAdd(counter, 1);
-    reinterpret_cast<volatile int*>(bar.item_ring)[slot] = it;
-    mbar_arrive(&bar.item_full[slot]);
-  }
-  return __shfl_sync(0xffffffffu, it, 0);
+  return x;
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
-    k1_prefill(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-               const __grid_constant__ CUtensorMap tmV, Params p) {
+    k1_prefill(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ KvHeadMaps maps, Params p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   Bars& bar = *reinterpret_cast<Bars*>(smem + kOffBar);
+  ItemSlot* ring = reinterpret_cast<ItemSlot*>(smem + kOffBar + kOffItems);
   const uint32_t sbase = smem_u32(smem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   PATTN_CTA_BEGIN(k1);
@@ -220,7 +255,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&bar.v_empty[s], 1);
     }
     for (int h = 0; h < 2; ++h) {
-      mbar_init(&bar.s_full[h], 1);
+      mbar_init(&bar.s_full[h][0], 1);
+      mbar_init(&bar.s_full[h][1], 1);
       mbar_init(&bar.p_full[h], kHalfM);
       mbar_init(&bar.pv_done[h], 1);
       mbar_init(&bar.o_empty[h], kHalfM);
@@ -257,35 +293,35 @@ __global__ void __launch_bounds__(kThreads, 1)
       asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
     const int kv = (warp == 3 || warp == 12) ? 1 : 0;
     const bool owner = warp == 0 || warp == 3;  // arms the stage barrier with the tile's byte count
-    const int i_lo = owner ? 0 : 4, i_hi = owner ? 4 : 8;
-    if (lane == 0) {
-      if (kv == 0) tma_prefetch_desc(&tmQ);
-      tma_prefetch_desc(kv ? &tmV : &tmK);
-    }
+    const int i_lo = owner ? 0 : kN / 32, i_hi = i_lo + kN / 32;  // 2 sub-blocks per warp
+    if (lane == 0 && kv == 0) tma_prefetch_desc(&tmQ);
     // A 128-key tile = 8 sub-blocks of 16 keys; sub-block idx is slots [(idx % n16)*16, +16)
-    // of paged block bt[idx / n16] (any block size that is a multiple of 16).
+    // of paged block bt[idx / n16] (any block size that is a multiple of 16).  One 4 KB TMA
+    // box per sub-block (per-head 5-D map); the warp's 4 boxes are issued by lanes 0-3
+    // together.
     constexpr int nbt = kN / 16;
     const int n16 = p.bs / 16;
     const uint64_t pol_kv = l2_policy_evict_last();  // K/V tiles are re-read by the sequence's other Q blocks
-    const CUtensorMap* tm = kv ? &tmV : &tmK;
     const int nst = kv ? kVStages : kKStages;
     uint32_t ic = 0, cnt = 0;
     for (;; ++ic) {
-      const int it = warp == 0 ? publish_item(bar, ic, lane, p.hdr + kHdrPrefillCounter) : next_item(bar, ic, lane);
-      if (it >= n_items) break;
-      const Item x = prefill_item(p, total_qb, it);
+      int id0;
+      const Item x = next_item(bar, ring, ic, lane, &id0);
+      if (x.ntiles < 0) break;
+      const CUtensorMap* tm = kv ? &maps.v[x.kvh] : &maps.k[x.kvh];
+      if (lane == 0) tma_prefetch_desc(tm);
       const int32_t* bt = p.block_table + (int64_t)x.b * p.bt_stride;
       const int nsb_valid = (x.kv_end + 15) / 16;  // sub-blocks holding visible keys
       if (warp == 0 && lane == 0) {
         mbar_wait(&bar.q_empty, (ic & 1u) ^ 1u);
-        mbar_arrive_expect_tx(&bar.q_full, 2 * kTile);
+        mbar_arrive_expect_tx(&bar.q_full, 2 * kQTile);
         for (int h = 0; h < 2; ++h) {
           const int tok = x.q0 + x.tok0 + h * bq_half;
-          tma_load_4d(smem + kOffQ + h * kTile, &tmQ, &bar.q_full, 0, 0, x.kvh, tok);
-          tma_load_4d(smem + kOffQ + h * kTile + kHalf, &tmQ, &bar.q_full, 64, 0, x.kvh, tok);
+          tma_load_4d(smem + kOffQ + h * kQTile, &tmQ, &bar.q_full, 0, 0, x.kvh, tok);
+          tma_load_4d(smem + kOffQ + h * kQTile + kHalf, &tmQ, &bar.q_full, 64, 0, x.kvh, tok);
         }
       }
-      int id_next = (lane < nbt && lane < nsb_valid) ? __ldg(bt + lane / n16) : p.num_blocks;
+      int id_next = id0;  // tile 0: fetched by the scheduler
       for (int jt = 0; jt < x.ntiles; ++jt) {
         const int id_cur = id_next;
         const int sb_next = (jt + 1) * nbt + lane;
@@ -294,26 +330,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint64_t* fullb = kv ? &bar.v_full[s] : &bar.k_full[s];
         uint64_t* emptyb = kv ? &bar.v_empty[s] : &bar.k_empty[s];
         uint8_t* base = smem + (kv ? kOffV : kOffK) + s * kTile;
+        const int i = i_lo + (lane & 1);
+        const int blk = __shfl_sync(0xffffffffu, id_cur, i);
         if (lane == 0) {
+          if (owner) PATTN_K1_TRACE(24 + kv);
           mbar_wait(emptyb, ph ^ 1u);
           if (owner) mbar_arrive_expect_tx(fullb, kTile);
+          if (owner) PATTN_K1_TRACE(20 + kv);
         }
-        for (int i = i_lo; i < i_hi; ++i) {
-          const int blk = __shfl_sync(0xffffffffu, id_cur, i);
-          const int slot0 = ((jt * nbt + i) % n16) * 16;
-          const int c1 = p.kv_tok_inner ? slot0 : x.kvh, c2 = p.kv_tok_inner ? x.kvh : slot0;
-          if (lane == 0) {
-            uint8_t* dst = base + i * 16 * 128;
-            if (i == i_lo && owner) PATTN_K1_TRACE(20 + kv);
-#ifdef PATTN_NO_L2HINT
-            tma_load_4d(dst, tm, fullb, 0, c1, c2, blk);
-            tma_load_4d(dst + kHalf, tm, fullb, 64, c1, c2, blk);
-#else
-            tma_load_4d_hint(dst, tm, fullb, 0, c1, c2, blk, pol_kv);
-            tma_load_4d_hint(dst + kHalf, tm, fullb, 64, c1, c2, blk, pol_kv);
-#endif
-          }
+        __syncwarp();
+        if (lane < kN / 32) {
+          const int grp0 = ((jt * nbt + i) % n16) * 2;  // first 8-slot group of the sub-block
+          tma_load_5d_hint(base + i * kSub16Bytes, tm, fullb, 0, 0, 0, grp0, blk, pol_kv);
         }
+        __syncwarp();
+        if (lane == 0 && owner) PATTN_K1_TRACE(22 + kv);
         ++cnt;
       }
     }
@@ -326,35 +357,58 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr uint32_t idPV = idesc_bf16_f32(kHalfM, kD, 0, 1);  // P (TMEM, K-major) x V (MN-major)
     // smem descriptors: start-address field = addr >> 4, so desc(base + off) = desc(base) + (off >> 4)
     const uint64_t dQ = smem_desc_sw128(sbase + kOffQ, 16, 1024);
-    const uint64_t dK = smem_desc_sw128(sbase + kOffK, 16, 1024);
-    const uint64_t dV = smem_desc_sw128(sbase + kOffV, kHalf, 1024);
+    const uint64_t dK = smem_desc_sw128(sbase + kOffK, 16, 2048);     // 8-key groups 2 KB apart
+    const uint64_t dV = smem_desc_sw128(sbase + kOffV, 1024, 2048);   // d halves 1 KB apart
     const bool leader = elect_one();
     uint32_t ic = 0, kc = 0, vc = 0;
     uint32_t pc[2] = {0u, 0u};
     for (;; ++ic) {
-      const int it = next_item(bar, ic, lane);
-      if (it >= n_items) break;
-      const Item x = prefill_item(p, total_qb, it);
+      const Item x = next_item(bar, ring, ic, lane);
+      if (x.ntiles < 0) break;
+      if (leader) PATTN_K1_TRACE(40);
       mbar_wait(&bar.q_full, ic & 1u);
+      if (leader) PATTN_K1_TRACE(41);
       tc_fence_after();
+      // Iteration jt: S_a(jt), S_b(jt) into S buffer jt&1 of each half, then PV_a(jt-1),
+      // PV_b(jt-1) from buffer (jt-1)&1.  S_h(jt) overwrites P_h(jt-2), whose PV was issued
+      // one iteration earlier (tcgen05 ops execute in issue order), so the softmax of tile
+      // jt overlaps the PV of tile jt-1 instead of waiting for it.
       for (int jt = 0; jt <= x.ntiles; ++jt) {
         const bool do_s = jt < x.ntiles, do_pv = jt > 0;
-        uint32_t ks = 0, vs = 0;
         if (do_s) {
-          ks = kc % kKStages;
+          const uint32_t ks = kc % kKStages;
           mbar_wait(&bar.k_full[ks], (kc / kKStages) & 1u);
           if (leader) PATTN_K1_TRACE(1);
+          tc_fence_after();
+          if (leader) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const uint32_t tS = tmem + kTmemS + 128 * h + 64 * (jt & 1);
+              const uint64_t dq = dQ + ((h * kQTile) >> 4), dk = dK + ((ks * kTile) >> 4);
+#pragma unroll
+              for (int k = 0; k < kD / 16; ++k) {
+                const uint32_t offq = ((k >> 2) * kHalf + (k & 3) * 32) >> 4;
+                const uint32_t offk = ((k >> 2) * 1024 + (k & 3) * 32) >> 4;
+#ifndef PATTN_K1_NOMMA  // timing experiment only: no tensor work
+                tc_mma_f16_ss(tS, dq + offq, dk + offk, idS, k > 0 ? 1u : 0u);
+#endif
+              }
+              PATTN_K1_TRACE(7 + h);
+              tc_commit(&bar.s_full[h][jt & 1]);
+            }
+            tc_commit(&bar.k_empty[ks]);
+            if (jt == x.ntiles - 1) tc_commit(&bar.q_empty);
+          }
+          __syncwarp();
+          ++kc;
         }
         if (do_pv) {
-          vs = vc % kVStages;
+          const uint32_t vs = vc % kVStages;
           mbar_wait(&bar.v_full[vs], (vc / kVStages) & 1u);
           if (leader) PATTN_K1_TRACE(2);
-        }
-        tc_fence_after();
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const uint32_t tS = tmem + kTmemS + 128 * h, tO = tmem + kTmemO + 128 * h;
-          if (do_pv) {  // PV_h(jt-1): P_h aliases S_h, so it must precede S_h(jt)
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t tP = tmem + kTmemS + 128 * h + 64 * ((jt - 1) & 1), tO = tmem + kTmemO + 128 * h;
             mbar_wait(&bar.p_full[h], pc[h] & 1u);
             if (jt == 1) mbar_wait(&bar.o_empty[h], (ic & 1u) ^ 1u);
             tc_fence_after();
@@ -362,77 +416,120 @@ __global__ void __launch_bounds__(kThreads, 1)
               PATTN_K1_TRACE(3 + h);
               const uint64_t dv = dV + ((vs * kTile) >> 4);
 #pragma unroll
-              for (int k = 0; k < kN / 16; ++k)
-                tc_mma_f16_ts(tO, tS + 8 * k, dv + ((k * 2048) >> 4), idPV, (jt > 1 || k > 0) ? 1u : 0u);
+              for (int k = 0; k < kN / 16; ++k) {
+#ifndef PATTN_K1_NOMMA
+                tc_mma_f16_ts(tO, tP + 8 * k, dv + ((k * kSub16Bytes) >> 4), idPV, (jt > 1 || k > 0) ? 1u : 0u);
+#endif
+              }
               PATTN_K1_TRACE(5 + h);
               tc_commit(&bar.pv_done[h]);
             }
             __syncwarp();
             ++pc[h];
           }
-          if (do_s) {  // S_h(jt) = Q_h K^T
-            if (leader) {
-              const uint64_t dq = dQ + ((h * kTile) >> 4), dk = dK + ((ks * kTile) >> 4);
-#pragma unroll
-              for (int k = 0; k < kD / 16; ++k) {
-                const uint32_t off = ((k >> 2) * kHalf + (k & 3) * 32) >> 4;
-                tc_mma_f16_ss(tS, dq + off, dk + off, idS, k > 0 ? 1u : 0u);
-              }
-              PATTN_K1_TRACE(7 + h);
-              tc_commit(&bar.s_full[h]);
-            }
-            __syncwarp();
-          }
+          if (leader) tc_commit(&bar.v_empty[vs]);
+          __syncwarp();
+          ++vc;
         }
-        if (leader) {
-          if (do_s) {
-            tc_commit(&bar.k_empty[ks]);
-            if (jt == x.ntiles - 1) tc_commit(&bar.q_empty);
-          }
-          if (do_pv) tc_commit(&bar.v_empty[vs]);
-        }
-        __syncwarp();
-        if (do_s) ++kc;
-        if (do_pv) ++vc;
       }
     }
   } else if (warp >= 13) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");  // spare warps of warpgroup 3
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");  // warpgroup 3
+    if (warp == 13) {
+      // ================================================================ item scheduler
+      const int n16 = p.bs / 16;
+      for (uint32_t n = 0;; ++n) {
+        const uint32_t slot = n % kItemRing;
+        int it = 0;
+        if (lane == 0) {
+          mbar_wait(&bar.item_empty[slot], ((n / kItemRing) & 1u) ^ 1u);
+          it = atomicAdd(p.hdr + kHdrPrefillCounter, 1);
+        }
+        it = __shfl_sync(0xffffffffu, it, 0);
+        volatile ItemSlot* e = ring + slot;
+        if (it < n_items) {
+          const Item x = prefill_item(p, total_qb, it);
+          const int nsb_valid = (x.kv_end + 15) / 16;
+          const int id = (lane < 8 && lane < nsb_valid) ? __ldg(p.block_table + (int64_t)x.b * p.bt_stride + lane / n16)
+                                                        : p.num_blocks;
+          int ids[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) ids[q] = __shfl_sync(0xffffffffu, id, q);
+          if (lane == 0) {  // one writer: program order before its release (the arrive below)
+#pragma unroll
+            for (int q = 0; q < 8; ++q) e->ids[q] = ids[q];
+            e->x.b = x.b;
+            e->x.kvh = x.kvh;
+            e->x.q0 = x.q0;
+            e->x.qlen = x.qlen;
+            e->x.L = x.L;
+            e->x.ctx = x.ctx;
+            e->x.tok0 = x.tok0;
+            e->x.ntok = x.ntok;
+            e->x.kv_end = x.kv_end;
+            e->x.ntiles = x.ntiles;
+          }
+        } else if (lane == 0) {
+          e->x.ntiles = -1;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bar.item_full[slot]);
+        if (it >= n_items) break;
+      }
+    }
   } else {
     // ================================================================ softmax / correction / epilogue
     asm volatile("setmaxnreg.inc.sync.aligned.u32 208;\n" ::: "memory");
     const int h = (warp - 4) >> 2;             // half a (0) or b (1)
     const int r = threadIdx.x - 128 - h * 128;  // row within the half == TMEM lane
     const uint32_t lane_off = (uint32_t)(32 * (warp & 3)) << 16;
-    const uint32_t tS = tmem + kTmemS + 128 * h + lane_off;
+    const uint32_t tS0 = tmem + kTmemS + 128 * h + lane_off;
     const uint32_t tO = tmem + kTmemO + 128 * h + lane_off;
     uint32_t tc = 0, vc = 0;  // tiles seen by this warpgroup (== PV count of this half)
+    uint32_t sc[2] = {0u, 0u};  // completed phases observed per S buffer
     __nv_bfloat16* O = static_cast<__nv_bfloat16*>(p.out);
     const float cs = p.scale_log2;
     const float ca = fmaxf(fabsf(cs), 1e-30f);  // scale 0: -inf * 0 would be NaN; 1e-30 * s ~ 0
     uint32_t ic = 0;
     for (;; ++ic) {
-      const int it = next_item(bar, ic, lane);
-      if (it >= n_items) break;
-      const Item x = prefill_item(p, total_qb, it);
+      const Item x = next_item(bar, ring, ic, lane);
+      if (x.ntiles < 0) break;
       const int tk = h * bq_half + r / G;  // token of this row within the Q block
       const bool row_valid = tk < x.ntok;
       const int row_lim = min(x.ctx + x.tok0 + tk + 1, x.kv_end);  // keys [0, row_lim) visible
       const int nsb_valid = (x.kv_end + 15) / 16;                  // 16-key sub-blocks fetched
       float m_run = -INFINITY, l_run = 0.f;
       for (int jt = 0; jt < x.ntiles; ++jt) {
-        mbar_wait(&bar.s_full[h], tc & 1u);
+        const int sb = jt & 1;  // S buffer of this tile (P is written back over it)
+        const uint32_t tS = tS0 + 64 * sb;
+        mbar_wait(&bar.s_full[h][sb], sc[sb] & 1u);
+        ++sc[sb];
         if (r == 0) PATTN_K1_TRACE(10 + h);
         tc_fence_after();
+#ifdef PATTN_K1_NOSOFTMAX  // timing experiment only: P = bf16 pairs of S, no max / exp / rescale
+        {
+          uint32_t pz[32];
+          PATTN_TMEM_LD32(tS + 0, pz);
+          tmem_wait_ld();
+          PATTN_TMEM_ST32(tS + 0, pz);
+          ++vc;
+          tmem_wait_st();
+          tc_fence_before();
+          mbar_arrive(&bar.p_full[h]);
+          ++tc;
+          l_run = 1.f;
+          if (jt > 0) mbar_wait(&bar.pv_done[h], (tc - 2) & 1u);
+          continue;
+        }
+#endif
         float s[kN];
         {
           uint32_t* su = reinterpret_cast<uint32_t*>(s);
           PATTN_TMEM_LD32(tS + 0, (su + 0));
           PATTN_TMEM_LD32(tS + 32, (su + 32));
-          PATTN_TMEM_LD32(tS + 64, (su + 64));
-          PATTN_TMEM_LD32(tS + 96, (su + 96));
           tmem_wait_ld();
         }
+        if (r == 0) PATTN_K1_TRACE(30 + h);
         const int key0 = jt * kN;
         const int nvis = row_lim - key0;  // keys [key0, key0 + nvis) of this tile are visible
         if (cs < 0.f) {  // sign-adjust so that max(raw) * |c| = max(scaled)
@@ -450,6 +547,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int c = 8; c < kN; ++c) mx[c & 7] = fmaxf(mx[c & 7], s[c]);
         const float mraw = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
                                  fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+        if (r == 0) PATTN_K1_TRACE(32 + h);
         const float mt = mraw * ca;
         const float m_new = fmaxf(m_run, mt);
         float alpha = 1.f, m_use = m_run;
@@ -467,15 +565,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int c = 0; c < kN; c += 2) {
           // e^{scale*qk - m} in the log2 domain
           const uint64_t xx = ffma2(f32x2(s[c], s[c + 1]), ca2, nb2);
-          const float e0 = fast_exp2(f32x2_lo(xx)), e1 = fast_exp2(f32x2_hi(xx));
-          const uint64_t ee = f32x2(e0, e1);
+          uint64_t ee;
+          float e0, e1;
+          if ((((c >> 1) & kPolyMask) == kPolyMask) && kPolyMask < 64) {  // this pair on the FMA pipe
+            ee = exp2_poly2(xx);
+            e0 = f32x2_lo(ee);
+            e1 = f32x2_hi(ee);
+          } else {
+            e0 = fast_exp2(f32x2_lo(xx));
+            e1 = fast_exp2(f32x2_hi(xx));
+            ee = f32x2(e0, e1);
+          }
           rs2[(c >> 1) & 3] = fadd2(rs2[(c >> 1) & 3], ee);
           pk[c >> 1] = pack_bf16(e0, e1);
         }
         const uint64_t r01 = fadd2(rs2[0], rs2[1]), r23 = fadd2(rs2[2], rs2[3]), rr = fadd2(r01, r23);
         const float rs = f32x2_lo(rr) + f32x2_hi(rr);
-        // O_h: PV_h(jt-1) was issued before S_h(jt) (in-order), so it is complete; the barrier
-        // wait orders its TMEM writes before our correction.
+        if (r == 0) PATTN_K1_TRACE(34 + h);
+        // O_h: PV_h(jt-1) (issued once P_h(jt-1) arrived, while this tile's exponentials ran)
+        // must be complete before O_h is corrected and before P_h(jt) can be consumed.
         if (jt > 0) {
           mbar_wait(&bar.pv_done[h], (tc - 1) & 1u);
           tc_fence_after();
@@ -494,9 +602,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         l_run = l_run * alpha + rs;
         m_run = m_use;
-        // P (bf16, 2 per column) over the first 64 columns of S_h: the A operand of PV_h
+        // P (bf16, 2 per column) over the first 32 columns of the S buffer: the A operand of PV_h
         PATTN_TMEM_ST32(tS + 0, (pk + 0));
-        PATTN_TMEM_ST32(tS + 32, (pk + 32));
         // WG a: zero V rows of slots >= L inside the last fetched sub-block (they may hold NaN)
         if (h == 0) {
           const int z0 = x.L - key0, z1 = min(kN, nsb_valid * 16 - key0);
@@ -506,7 +613,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint8_t* vb = smem + kOffV + s2 * kTile;
             for (int e = r; e < (z1 - z0) * 16; e += kHalfM) {
               const int row = z0 + (e >> 4), ch = e & 15;
-              *reinterpret_cast<uint4*>(vb + (ch >> 3) * kHalf + row * 128 + ((ch & 7) << 4)) = make_uint4(0, 0, 0, 0);
+              *reinterpret_cast<uint4*>(vb + (row >> 3) * 2048 + (ch >> 3) * 1024 + (row & 7) * 128 + ((ch & 7) << 4)) =
+                  make_uint4(0, 0, 0, 0);
             }
             fence_proxy_async_smem();
           }
@@ -520,29 +628,38 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       // ---- epilogue: O / l -> bf16 -> out (valid rows only)
       mbar_wait(&bar.pv_done[h], (tc - 1) & 1u);
+      if (r == 0) PATTN_K1_TRACE(42 + h);
       tc_fence_after();
       const float inv = 1.f / l_run;
       __nv_bfloat16* orow =
           O + (int64_t)(x.q0 + x.tok0 + tk) * p.o_st_tok + (int64_t)(x.kvh * G + (r % G)) * p.o_st_head;
-#pragma unroll
-      for (int c0 = 0; c0 < kD; c0 += 32) {
-        uint32_t o[32];
-        PATTN_TMEM_LD32(tO + c0, o);
-        tmem_wait_ld();
-        if (row_valid) {
-#pragma unroll
-          for (int c = 0; c < 32; c += 8) {
-            uint4 v;
-            v.x = pack_bf16(__uint_as_float(o[c + 0]) * inv, __uint_as_float(o[c + 1]) * inv);
-            v.y = pack_bf16(__uint_as_float(o[c + 2]) * inv, __uint_as_float(o[c + 3]) * inv);
-            v.z = pack_bf16(__uint_as_float(o[c + 4]) * inv, __uint_as_float(o[c + 5]) * inv);
-            v.w = pack_bf16(__uint_as_float(o[c + 6]) * inv, __uint_as_float(o[c + 7]) * inv);
-            *reinterpret_cast<uint4*>(orow + c0 + c) = v;
-          }
-        }
-      }
+      // all 128 columns of the O row in one go, then O_h is released to the next item's
+      // PV_h(0) before the normalisation and the global stores
+      uint32_t o[kD];
+      PATTN_TMEM_LD32(tO + 0, (o + 0));
+      PATTN_TMEM_LD32(tO + 32, (o + 32));
+      PATTN_TMEM_LD32(tO + 64, (o + 64));
+      PATTN_TMEM_LD32(tO + 96, (o + 96));
+      tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(&bar.o_empty[h]);
+      if (row_valid) {
+        const uint64_t inv2 = f32x2(inv, inv);
+#pragma unroll
+        for (int c = 0; c < kD; c += 8) {
+          uint4 v;
+          uint64_t a = fmul2((uint64_t)o[c + 0] | ((uint64_t)o[c + 1] << 32), inv2);
+          v.x = pack_bf16(f32x2_lo(a), f32x2_hi(a));
+          a = fmul2((uint64_t)o[c + 2] | ((uint64_t)o[c + 3] << 32), inv2);
+          v.y = pack_bf16(f32x2_lo(a), f32x2_hi(a));
+          a = fmul2((uint64_t)o[c + 4] | ((uint64_t)o[c + 5] << 32), inv2);
+          v.z = pack_bf16(f32x2_lo(a), f32x2_hi(a));
+          a = fmul2((uint64_t)o[c + 6] | ((uint64_t)o[c + 7] << 32), inv2);
+          v.w = pack_bf16(f32x2_lo(a), f32x2_hi(a));
+          *reinterpret_cast<uint4*>(orow + c) = v;
+        }
+      }
+      if (r == 0) PATTN_K1_TRACE(44 + h);
     }
     if (threadIdx.x == 128) PATTN_CTA_END(k1, ic);
   }
@@ -558,7 +675,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 bool prefill_supported(const Params& p) {
   if (getenv("PATTN_DISABLE_K1")) return false;
   // BLOCK_Q = 256/G tokens split into two halves of 128 rows: G must divide 128
-  return p.D == kD && p.G >= 1 && p.G <= kHalfM && (kHalfM % p.G) == 0 && p.bs % 16 == 0;
+  return p.D == kD && p.G >= 1 && p.G <= kHalfM && (kHalfM % p.G) == 0 && p.bs % 16 == 0 &&
+         p.Hkv <= kMaxKvHeadMaps;
 }
 
 int prefill_block_q(int G) { return kM / G; }
@@ -571,11 +689,11 @@ PrefillLaunch plan_prefill(const Params& p, int num_sms) {
   return pl;
 }
 
-cudaError_t launch_prefill(const Params& p, const PrefillLaunch& pl, const CUtensorMap& tmQ, const CUtensorMap& tmK,
-                           const CUtensorMap& tmV, cudaStream_t stream) {
+cudaError_t launch_prefill(const Params& p, const PrefillLaunch& pl, const CUtensorMap& tmQ, const KvHeadMaps& kv,
+                           cudaStream_t stream) {
   cudaError_t e = cudaFuncSetAttribute(k1_prefill, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
   if (e != cudaSuccess) return e;
-  k1_prefill<<<pl.grid, kThreads, pl.smem, stream>>>(tmQ, tmK, tmV, p);
+  k1_prefill<<<pl.grid, kThreads, pl.smem, stream>>>(tmQ, kv, p);
   return cudaGetLastError();
 }
 

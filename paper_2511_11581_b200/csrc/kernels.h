@@ -30,6 +30,14 @@ cudaError_t launch_decode(const Params& p, const DecodeLaunch& dl, const CUtenso
 cudaError_t launch_reduce(const Params& p, cudaStream_t stream);
 
 // K1: tcgen05/TMEM prefill Q-block kernel (bf16, D = 128).
+// Per-KV-head 5-D views of the K and V caches {64 d, 8 slots, 2 d-halves, bs/8 slot groups,
+// block}, box {64, 8, 2, 2, 1}: one TMA box = one 16-key sub-block of one head, landing as
+// [slot group][d half][8 slots][64 d] (4 KB), which UMMA reads with SBO = 2048.
+constexpr int kMaxKvHeadMaps = 64;
+struct KvHeadMaps {
+  CUtensorMap k[kMaxKvHeadMaps];
+  CUtensorMap v[kMaxKvHeadMaps];
+};
 struct PrefillLaunch {
   int grid;
   size_t smem;
@@ -37,7 +45,7 @@ struct PrefillLaunch {
 bool prefill_supported(const Params& p);
 int prefill_block_q(int G);  // tokens per K1 Q block (BLOCK_M / G)
 PrefillLaunch plan_prefill(const Params& p, int num_sms);
-cudaError_t launch_prefill(const Params& p, const PrefillLaunch& pl, const CUtensorMap& tmQ, const CUtensorMap& tmK,
-                           const CUtensorMap& tmV, cudaStream_t stream);
+cudaError_t launch_prefill(const Params& p, const PrefillLaunch& pl, const CUtensorMap& tmQ, const KvHeadMaps& kv,
+                           cudaStream_t stream);
 
 }  // namespace pattn

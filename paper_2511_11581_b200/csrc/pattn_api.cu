@@ -224,38 +224,58 @@ pattn_status_t make_plan(const pattn_problem_t* p, const void* q, const void* kc
   return PATTN_OK;
 }
 
-// H2: 4-D tensor map over one paged cache: dims ordered by stride so they nest.
-bool encode_kv_map(CUtensorMap* tm, const pattn_problem_t* p, const void* base, bool tok_inner) {
+// H2: per-KV-head 5-D views for K1 {64 d, 8 slots, 2 d-halves, bs/8 slot groups, block}
+// (the head is folded into the base address; strides deliberately not nested) so that one
+// box {64, 8, 2, 2, 1} brings a 16-key sub-block in the [group][half][8][64] order UMMA
+// reads with a uniform 2 KB stride between 8-key groups.  The maps of the last call are
+// cached (the encode is ~1 us of host time per map).
+bool encode_head_map(CUtensorMap* tm, const pattn_problem_t* p, const void* head_base) {
   auto fn = encode_fn();
   if (!fn) return false;
-  cuuint64_t dims[4];
-  cuuint64_t strides[3];
-  cuuint32_t box[4];
-  cuuint32_t estr[4] = {1, 1, 1, 1};
-  dims[0] = (cuuint64_t)p->head_dim;
-  if (tok_inner) {
-    dims[1] = (cuuint64_t)p->block_size;
-    dims[2] = (cuuint64_t)p->num_kv_heads;
-    strides[0] = (cuuint64_t)p->kv_stride_tok * 2;
-    strides[1] = (cuuint64_t)p->kv_stride_head * 2;
-    box[1] = 16;  // one 16-key sub-block of a paged block
-    box[2] = 1;
-  } else {
-    dims[1] = (cuuint64_t)p->num_kv_heads;
-    dims[2] = (cuuint64_t)p->block_size;
-    strides[0] = (cuuint64_t)p->kv_stride_head * 2;
-    strides[1] = (cuuint64_t)p->kv_stride_tok * 2;
-    box[1] = 1;
-    box[2] = 16;  // one 16-key sub-block of a paged block
-  }
-  dims[3] = (cuuint64_t)p->num_blocks;
-  strides[2] = (cuuint64_t)p->kv_stride_blk * 2;
-  box[0] = 64;
-  box[3] = 1;
-  CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, estr,
+  cuuint64_t dims[5] = {64, 8, (cuuint64_t)(p->head_dim / 64), (cuuint64_t)(p->block_size / 8),
+                        (cuuint64_t)p->num_blocks};
+  cuuint64_t strides[4] = {(cuuint64_t)p->kv_stride_tok * 2, 128, (cuuint64_t)p->kv_stride_tok * 2 * 8,
+                           (cuuint64_t)p->kv_stride_blk * 2};
+  cuuint32_t box[5] = {64, 8, (cuuint32_t)(p->head_dim / 64), 2, 1};
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(head_base), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
+}
+
+struct HeadMapCache {
+  std::mutex mu;
+  bool valid = false;
+  const void* k = nullptr;
+  const void* v = nullptr;
+  pattn_problem_t prob{};
+  KvHeadMaps maps;
+};
+
+bool encode_head_maps(KvHeadMaps* out, const pattn_problem_t* p, const void* kc, const void* vc) {
+  static HeadMapCache cache;
+  std::lock_guard<std::mutex> lock(cache.mu);
+  const bool hit = cache.valid && cache.k == kc && cache.v == vc && cache.prob.num_kv_heads == p->num_kv_heads &&
+                   cache.prob.head_dim == p->head_dim && cache.prob.block_size == p->block_size &&
+                   cache.prob.num_blocks == p->num_blocks && cache.prob.kv_stride_blk == p->kv_stride_blk &&
+                   cache.prob.kv_stride_tok == p->kv_stride_tok && cache.prob.kv_stride_head == p->kv_stride_head;
+  if (!hit) {
+    cache.valid = false;
+    for (int h = 0; h < p->num_kv_heads; ++h) {
+      const int64_t off = (int64_t)h * p->kv_stride_head * 2;
+      if (!encode_head_map(&cache.maps.k[h], p, static_cast<const uint8_t*>(kc) + off) ||
+          !encode_head_map(&cache.maps.v[h], p, static_cast<const uint8_t*>(vc) + off))
+        return false;
+    }
+    cache.k = kc;
+    cache.v = vc;
+    cache.prob = *p;
+    cache.valid = true;
+  }
+  memcpy(out->k, cache.maps.k, sizeof(CUtensorMap) * p->num_kv_heads);
+  memcpy(out->v, cache.maps.v, sizeof(CUtensorMap) * p->num_kv_heads);
+  return true;
 }
 
 // H2b: 5-D view {64 d, slot, D/64 d-halves, head, block} (strides deliberately not nested:
@@ -338,14 +358,14 @@ pattn_status_t run(const pattn_problem_t* p, const void* q, const void* k_cache,
   k.part_l = reinterpret_cast<float*>(ws + pl.off_pl);
   k.part_acc = reinterpret_cast<float*>(ws + pl.off_pacc);
 
-  CUtensorMap tmK, tmV, tmQ, tmK5, tmV5;
+  CUtensorMap tmQ, tmK5, tmV5;
+  static thread_local KvHeadMaps head_maps;  // 16 KB: kept off the stack
   if (!metadata_only) {
     if (pl.use_k2) {
       if (!encode_kv_map5(&tmK5, p, k_cache) || !encode_kv_map5(&tmV5, p, v_cache)) return PATTN_ERR_UNSUPPORTED;
     }
     if (pl.use_k1) {
-      if (!encode_kv_map(&tmK, p, k_cache, pl.kv_tok_inner) || !encode_kv_map(&tmV, p, v_cache, pl.kv_tok_inner))
-        return PATTN_ERR_UNSUPPORTED;
+      if (!encode_head_maps(&head_maps, p, k_cache, v_cache)) return PATTN_ERR_UNSUPPORTED;
     }
     if (pl.use_k1) {
       if (!encode_q_map(&tmQ, p, q, pl.block_q)) return PATTN_ERR_UNSUPPORTED;
@@ -385,7 +405,7 @@ pattn_status_t run(const pattn_problem_t* p, const void* q, const void* k_cache,
   // the prefill CTAs release when they finish.
   if (pl.use_k1) {
     ev.rec(2 * PATTN_KERNEL_PREFILL, s1);
-    e = launch_prefill(k, pl.pl, tmQ, tmK, tmV, s1);
+    e = launch_prefill(k, pl.pl, tmQ, head_maps, s1);
     ev.rec(2 * PATTN_KERNEL_PREFILL + 1, s1);
     if (e != cudaSuccess) return cuda_fail(e);
   }

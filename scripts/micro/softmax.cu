@@ -1,0 +1,78 @@
+// Microbenchmark: the K1 per-tile softmax arithmetic alone (no TMEM, no barriers): 64 scores
+// per thread -> max, exp2 (MUFU or part polynomial), packed row sum, bf16 pack.
+// One CTA per SM with W warps (W/4 per SMSP); reports clk per tile per warp.
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+__device__ __forceinline__ uint64_t f2(float a, float b) { uint64_t r; asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b)); return r; }
+__device__ __forceinline__ float lo(uint64_t v) { return __uint_as_float((uint32_t)v); }
+__device__ __forceinline__ float hi(uint64_t v) { return __uint_as_float((uint32_t)(v >> 32)); }
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) { uint64_t d; asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c)); return d; }
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) { uint64_t d; asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b)); return d; }
+__device__ __forceinline__ float ex2(float x) { float y; asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
+__device__ __forceinline__ uint32_t pk(float a, float b) { uint32_t r; asm("cvt.rn.bf16x2.f32 %0, %2, %1;" : "=r"(r) : "f"(a), "f"(b)); return r; }
+__device__ __forceinline__ uint64_t poly2(uint64_t xx) {
+  const uint64_t x = f2(fmaxf(lo(xx), -127.f), fmaxf(hi(xx), -127.f));
+  const uint64_t t = fadd2(x, f2(12582912.f, 12582912.f));
+  const uint64_t n = fadd2(t, f2(-12582912.f, -12582912.f));
+  const uint64_t f = fadd2(x, n ^ 0x8000000080000000ull);
+  uint64_t p = ffma2(f2(0.0550085f, 0.0550085f), f, f2(0.2422103f, 0.2422103f));
+  p = ffma2(p, f, f2(0.6932829f, 0.6932829f));
+  p = ffma2(p, f, f2(1.f, 1.f));
+  const uint32_t l = (uint32_t)p + ((uint32_t)t << 23), h = (uint32_t)(p >> 32) + ((uint32_t)(t >> 32) << 23);
+  return (uint64_t)l | ((uint64_t)h << 32);
+}
+template <int MASK>
+__global__ void k(const float* in, uint32_t* out, int tiles, long long* clk) {
+  float s[64];
+  for (int c = 0; c < 64; ++c) s[c] = in[(threadIdx.x * 64 + c) & 4095];
+  uint32_t acc = 0;
+  float m_run = -1e30f, l_run = 0.f;
+  long long t0 = clock64();
+  for (int j = 0; j < tiles; ++j) {
+    float mx[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) mx[i] = s[i];
+#pragma unroll
+    for (int c = 8; c < 64; ++c) mx[c & 7] = fmaxf(mx[c & 7], s[c]);
+    const float mraw = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])), fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+    const float m_new = fmaxf(m_run, mraw * 0.125f);
+    const uint64_t ca2 = f2(0.125f, 0.125f), nb2 = f2(-m_new, -m_new);
+    uint64_t rs2[4] = {0, 0, 0, 0};
+    uint32_t p[32];
+#pragma unroll
+    for (int c = 0; c < 64; c += 2) {
+      const uint64_t xx = ffma2(f2(s[c], s[c + 1]), ca2, nb2);
+      uint64_t ee;
+      float e0, e1;
+      if (((c >> 1) & MASK) == MASK && MASK < 64) { ee = poly2(xx); e0 = lo(ee); e1 = hi(ee); }
+      else { e0 = ex2(lo(xx)); e1 = ex2(hi(xx)); ee = f2(e0, e1); }
+      rs2[(c >> 1) & 3] = fadd2(rs2[(c >> 1) & 3], ee);
+      p[c >> 1] = pk(e0, e1);
+    }
+    const uint64_t rr = fadd2(fadd2(rs2[0], rs2[1]), fadd2(rs2[2], rs2[3]));
+    l_run = l_run + lo(rr) + hi(rr);
+    m_run = m_new;
+#pragma unroll
+    for (int c = 0; c < 32; ++c) acc ^= p[c];
+#pragma unroll
+    for (int c = 0; c < 64; ++c) s[c] = __uint_as_float(__float_as_uint(s[c]) ^ (acc & 1));  // new "tile"
+  }
+  long long t1 = clock64();
+  out[blockIdx.x * blockDim.x + threadIdx.x] = acc + __float_as_uint(l_run);
+  if (threadIdx.x == 0) clk[blockIdx.x] = t1 - t0;
+}
+template <int MASK> void run(int warps) {
+  float* in; uint32_t* out; long long* c;
+  cudaMalloc(&in, 4096 * 4); cudaMemset(in, 0, 4096 * 4);
+  cudaMalloc(&out, 148 * 1024 * 4); cudaMalloc(&c, 148 * 8);
+  const int tiles = 2000;
+  k<MASK><<<148, warps * 32>>>(in, out, tiles, c); cudaDeviceSynchronize();
+  k<MASK><<<148, warps * 32>>>(in, out, tiles, c); cudaDeviceSynchronize();
+  long long h; cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost);
+  printf("mask %3d warps/SM %2d (%d per SMSP): %.0f clk per tile per warp\n", MASK, warps, warps / 4, (double)h / tiles);
+}
+int main() {
+  for (int w : {4, 8, 16}) { run<255>(w); run<7>(w); run<3>(w); run<1>(w); }
+  return 0;
+}
