@@ -56,6 +56,12 @@ def parse():
                     help="2 (default): decode kernels on a second stream, concurrent with prefill; 1: serial")
     ap.add_argument("--flags", type=int, default=0)
     ap.add_argument("--seed", type=int, default=3003)
+    ap.add_argument("--shard", default="none", choices=["none", "seq", "kvhead"],
+                    help="N>1: split ONE global batch of the workload over the ranks (strong scaling; "
+                         "shard.py plan); none = every rank runs the full workload (weak scaling)")
+    ap.add_argument("--sim-world", type=int, default=0,
+                    help="with --shard: run rank --sim-rank of a --sim-world-way shard on this one GPU")
+    ap.add_argument("--sim-rank", type=int, default=0)
     return ap.parse_args()
 
 
@@ -227,7 +233,7 @@ def run_reference(args):
         "warmup": args.warmup,
         "ms_per_step": 1e3 * tot_t / args.steps,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "weak" if args.shard == "none" else "strong",
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic",
@@ -252,7 +258,7 @@ def main():
 
     from paper_2511_11581_b200 import pattn
     from workloads import CONFIGS
-    from workloads.gen import generate_device
+    from workloads.gen import ATTRIBUTION, generate_device
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -263,7 +269,10 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     pattn.load()
 
-    w = CONFIGS[args.workload]
+    w_global = CONFIGS[args.workload] if args.workload in CONFIGS else ATTRIBUTION[args.workload]
+    shard_world = args.sim_world if args.sim_world else world
+    shard_rank = args.sim_rank if args.sim_world else rank
+    w = local_workload(w_global, args.shard, shard_world, shard_rank)
     inp = generate_device(w, seed=args.seed + rank, device=dev)
     q, kc, vc = inp["q"], inp["k_cache"], inp["v_cache"]
     bt, cu, sl = inp["block_table"], inp["cu_seqlens_q"], inp["seq_lens"]
@@ -311,6 +320,13 @@ def main():
         if kmask & (1 << k):
             kern_ms[pattn.KERNEL_NAMES[k]] = sum(kev[i][2 * k].elapsed_time(kev[i][2 * k + 1]) for i in range(K)) / K
 
+    if args.shard == "none":
+        tokens_all = w.num_tokens * world  # weak scaling: every rank runs the full workload
+    elif args.sim_world:
+        tokens_all = w.num_tokens if args.shard == "seq" else w.num_tokens / args.sim_world  # this rank's share
+    else:
+        tokens_all = w_global.num_tokens  # strong scaling: one global batch split over the ranks
+
     # ---------------- the same step captured once as a CUDA graph and replayed (static grids,
     # device-resident metadata: P:190-199); reported beside the eager number
     graph = None
@@ -346,7 +362,7 @@ def main():
         cg.replay()
         torch.cuda.synchronize()
         same = bool(torch.equal(out, ref_out))
-        graph = {"ms_per_step": float(gms.item()), "value": w.num_tokens * world / (float(gms.item()) * 1e-3),
+        graph = {"ms_per_step": float(gms.item()), "value": tokens_all / (float(gms.item()) * 1e-3),
                  "replay_matches_eager": same}
     except Exception as ex:  # reported, never fatal
         graph = {"error": str(ex)[:200]}
@@ -355,7 +371,6 @@ def main():
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms_max = float(ms_t.item())
-    tokens_all = w.num_tokens * world
     value = tokens_all / (ms_max * 1e-3)
 
     # ---------------- e2e through the host-buffer C-ABI call
@@ -432,7 +447,7 @@ def main():
         "warmup": max(3, args.warmup),
         "ms_per_step": ms_max,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "weak" if args.shard == "none" else "strong",
         "vs_baseline": None,
         "dtype": "bf16" if w.dtype == "bf16" else "f32",
         "data": "synthetic",
@@ -443,7 +458,7 @@ def main():
             "heads": f"{w.num_q_heads}q/{w.num_kv_heads}kv x d{w.head_dim}",
             "block_size": w.block_size,
             "tokens_per_step_per_gpu": w.num_tokens,
-            "parallelism": f"dp{world} (sequence-sharded batches, no collective)",
+            "parallelism": parallelism_text(args, world, w_global, w),
             "l2": "inputs > L2 (KV cache %.2f GB/GPU), no flush" % (kc.numel() * 2 * kc.element_size() / 1e9),
             "streams": args.streams,
             "flags": args.flags,
@@ -467,6 +482,33 @@ def main():
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def local_workload(w, mode, world, rank):
+    """This rank's share of ONE global batch (shard.py plan).  Mode "seq": the
+    rank's sequences (class-aware LPT balance); "kvhead": the rank's Hkv/P KV heads and their
+    query heads for every sequence.  Mode "none" or world 1: the workload itself."""
+    if mode == "none" or world <= 1:
+        return w
+    from paper_2511_11581_b200 import shard
+
+    q_lens = np.array([q for _, q in w.seqs], np.int64)
+    cu = np.concatenate([[0], np.cumsum(q_lens)])
+    sl = np.array([c + q for c, q in w.seqs], np.int64)
+    plan = shard.plan_shards(cu, sl, w.num_q_heads, w.num_kv_heads, w.head_dim, world, mode)
+    if mode == "kvhead":
+        return w.__class__(f"{w.name}/kvhead{rank}of{world}", w.seqs, len(plan.q_heads[rank]),
+                           len(plan.kv_heads[rank]), w.head_dim, w.block_size, w.dtype)
+    return w.with_seqs([w.seqs[b] for b in plan.seq_ids[rank]], name=f"{w.name}/seq{rank}of{world}")
+
+
+def parallelism_text(args, world, w_global, w):
+    if args.shard == "none":
+        return f"dp{world} (every rank runs the full workload; no collective)"
+    if args.sim_world:
+        return (f"{args.shard}-shard rank {args.sim_rank} of {args.sim_world} run alone on 1 GPU "
+                f"({w.num_seqs} seqs, {w.num_q_heads}q/{w.num_kv_heads}kv heads; value = this rank's tokens/s)")
+    return f"{args.shard}-sharded global batch over {world} ranks (strong scaling; no collective)"
 
 
 def load_traffic(workload):

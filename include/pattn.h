@@ -181,6 +181,30 @@ PATTN_API pattn_status_t pattn_unified_attention_hostio(const pattn_problem_t* p
                                               float scale, void* out_host, void* workspace,
                                               size_t workspace_bytes, void* stream);
 
+/*
+ * Paged KV write ("reshape and cache"): store the K and V rows of the batch's query
+ * tokens into the paged caches, the step the attention call presupposes ("Q, K, and V
+ * have already been computed ... and stored in the KV cache in blocks", §4.3
+ * P:327, App. A; SPEC write_kv S:139-147).  For sequence b, token i in [0, q_b):
+ *     pos = L_b - q_b + i ;  blk = block_table[b][pos / block_size] ;  slot = pos % block_size
+ *     k_cache[blk][slot][h][:] = k_new[cu_seqlens_q[b] + i][h][:]   (h < num_kv_heads; same for V)
+ * i.e. the same batch metadata as pattn_unified_attention, so a caller runs
+ * pattn_write_kv then pattn_unified_attention on one stream.  A bit-exact copy.
+ *   p:       uses num_seqs, num_tokens, num_kv_heads, head_dim, block_size, dtype,
+ *            max_blocks_per_seq, kv_stride_*, bt_stride (the q/o fields are ignored).
+ *   k_new, v_new: DEVICE [num_tokens][num_kv_heads][head_dim], strides
+ *            (new_stride_tok, new_stride_head, 1) in elements, shared by both.
+ *   k_cache, v_cache: DEVICE caches, written only at the addressed (blk, slot) rows.
+ * Every row start must be 16-byte aligned (else PATTN_ERR_UNSUPPORTED).  Metadata is
+ * trusted as in pattn_unified_attention (validate with pattn_validate_metadata_host);
+ * two tokens addressing the same (blk, slot) is a caller error (last writer undefined).
+ * num_tokens == 0 is a no-op.  Asynchronous on `stream`.
+ */
+PATTN_API pattn_status_t pattn_write_kv(const pattn_problem_t* p, const void* k_new, const void* v_new,
+                                        int64_t new_stride_tok, int64_t new_stride_head, void* k_cache,
+                                        void* v_cache, const int32_t* block_table, const int32_t* cu_seqlens_q,
+                                        const int32_t* seq_lens, void* stream);
+
 /* Static string for a status code. */
 PATTN_API const char* pattn_status_string(pattn_status_t s);
 

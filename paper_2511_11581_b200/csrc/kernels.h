@@ -48,4 +48,21 @@ PrefillLaunch plan_prefill(const Params& p, int num_sms);
 cudaError_t launch_prefill(const Params& p, const PrefillLaunch& pl, const CUtensorMap& tmQ, const KvHeadMaps& kv,
                            cudaStream_t stream);
 
+// K6: paged KV write (reshape-and-cache).  Strides in BYTES; every row start and row_bytes
+// are multiples of 16 (checked by the API).
+struct WriteKvParams {
+  const void* k_new;
+  const void* v_new;
+  void* k_cache;
+  void* v_cache;
+  const int32_t* block_table;
+  const int32_t* cu_seqlens_q;
+  const int32_t* seq_lens;
+  int32_t B, T, Hkv, bs, row_bytes;
+  int64_t new_st_tok, new_st_head;
+  int64_t kv_st_blk, kv_st_tok, kv_st_head;
+  int64_t bt_stride;  // elements
+};
+cudaError_t launch_write_kv(const WriteKvParams& p, int num_sms, cudaStream_t stream);
+
 }  // namespace pattn

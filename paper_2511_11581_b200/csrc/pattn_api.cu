@@ -596,6 +596,50 @@ int32_t pattn_planned_kernels(const pattn_problem_t* p) {
          (pl.use_k4 ? 1 << PATTN_KERNEL_GENERIC : 0);
 }
 
+pattn_status_t pattn_write_kv(const pattn_problem_t* p, const void* k_new, const void* v_new,
+                              int64_t new_stride_tok, int64_t new_stride_head, void* k_cache, void* v_cache,
+                              const int32_t* block_table, const int32_t* cu_seqlens_q, const int32_t* seq_lens,
+                              void* stream) {
+  if (!p) return PATTN_ERR_INVALID_ARG;
+  if (p->num_seqs <= 0) return PATTN_ERR_EMPTY_BATCH;
+  if (p->num_tokens < 0 || p->num_kv_heads <= 0 || p->block_size <= 0 || p->head_dim <= 0 ||
+      p->max_blocks_per_seq <= 0 || p->bt_stride < p->max_blocks_per_seq || new_stride_tok <= 0 ||
+      new_stride_head <= 0 || p->kv_stride_blk <= 0 || p->kv_stride_tok <= 0 || p->kv_stride_head <= 0)
+    return PATTN_ERR_INVALID_ARG;
+  if (p->dtype != PATTN_DTYPE_F32 && p->dtype != PATTN_DTYPE_BF16) return PATTN_ERR_UNSUPPORTED;
+  if (p->num_tokens == 0) return PATTN_OK;
+  if (!k_new || !v_new || !k_cache || !v_cache || !block_table || !cu_seqlens_q || !seq_lens)
+    return PATTN_ERR_INVALID_ARG;
+  const int64_t esz = p->dtype == PATTN_DTYPE_BF16 ? 2 : 4;
+  WriteKvParams w{};
+  w.k_new = k_new;
+  w.v_new = v_new;
+  w.k_cache = k_cache;
+  w.v_cache = v_cache;
+  w.block_table = block_table;
+  w.cu_seqlens_q = cu_seqlens_q;
+  w.seq_lens = seq_lens;
+  w.B = p->num_seqs;
+  w.T = p->num_tokens;
+  w.Hkv = p->num_kv_heads;
+  w.bs = p->block_size;
+  w.row_bytes = (int32_t)(p->head_dim * esz);
+  w.new_st_tok = new_stride_tok * esz;
+  w.new_st_head = new_stride_head * esz;
+  w.kv_st_blk = p->kv_stride_blk * esz;
+  w.kv_st_tok = p->kv_stride_tok * esz;
+  w.kv_st_head = p->kv_stride_head * esz;
+  w.bt_stride = p->bt_stride;
+  // 16-byte vector moves: every row start must be 16-B aligned
+  if ((w.row_bytes | w.new_st_tok | w.new_st_head | w.kv_st_blk | w.kv_st_tok | w.kv_st_head) & 15 ||
+      !aligned16(k_new) || !aligned16(v_new) || !aligned16(k_cache) || !aligned16(v_cache))
+    return PATTN_ERR_UNSUPPORTED;
+  const DeviceInfo di = device_info();
+  if (!di.ok) return cuda_fail(cudaGetLastError());
+  const cudaError_t e = launch_write_kv(w, di.sms, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? PATTN_OK : cuda_fail(e);
+}
+
 int32_t pattn_version(void) { return kVersion; }
 
 const char* pattn_last_error(void) { return g_last_error; }

@@ -88,6 +88,7 @@ EXPORTS = [
     "pattn_planned_kernels",
     "pattn_last_error",
     "pattn_version",
+    "pattn_write_kv",
 ]
 
 
@@ -122,6 +123,9 @@ def load() -> ctypes.CDLL:
             lib.pattn_planned_launches.argtypes = [P]
             lib.pattn_planned_kernels.restype = ctypes.c_int32
             lib.pattn_planned_kernels.argtypes = [P]
+            if hasattr(lib, "pattn_write_kv"):  # absent only in older A/B builds (PATTN_LIB)
+                lib.pattn_write_kv.restype = ctypes.c_int
+                lib.pattn_write_kv.argtypes = [P, vp, vp, ctypes.c_int64, ctypes.c_int64, vp, vp, vp, vp, vp, vp]
             lib.pattn_version.restype = ctypes.c_int32
             lib.pattn_last_error.restype = ctypes.c_char_p
             _lib = lib
@@ -306,6 +310,39 @@ def unified_attention_hostio(
         "pattn_unified_attention_hostio",
     )
     return out_host
+
+
+def write_kv(
+    k_new: torch.Tensor,
+    v_new: torch.Tensor,
+    k_cache: torch.Tensor,
+    v_cache: torch.Tensor,
+    block_table: torch.Tensor,
+    cu_seqlens_q: torch.Tensor,
+    seq_lens: torch.Tensor,
+    block_size: int,
+    *,
+    kv_layout: str = "NHD",
+    stream: Optional[torch.cuda.Stream] = None,
+) -> None:
+    """Paged KV write (pattn_write_kv): store k_new / v_new [T, Hkv, D] rows of the batch's query
+    tokens into the caches at positions ctx_b + i through the block table.  Enqueued on `stream`."""
+    lib = load()
+    if k_new.shape != v_new.shape or k_new.stride() != v_new.stride() or k_new.stride(2) != 1:
+        raise PattnError(1, "k_new/v_new shape/stride mismatch")
+    if k_cache.shape != v_cache.shape or k_cache.stride() != v_cache.stride():
+        raise PattnError(1, "k_cache/v_cache shape/stride mismatch")
+    if k_new.dtype != k_cache.dtype:
+        raise PattnError(1, "dtype mismatch")
+    T, hkv, _ = k_new.shape
+    p = make_problem(k_new, k_cache, hkv, block_size, block_table, seq_lens.shape[0], None, kv_layout)
+    s = stream if stream is not None else torch.cuda.current_stream(k_cache.device)
+    _check(
+        lib.pattn_write_kv(ctypes.byref(p), k_new.data_ptr(), v_new.data_ptr(), k_new.stride(0), k_new.stride(1),
+                           k_cache.data_ptr(), v_cache.data_ptr(), block_table.data_ptr(), cu_seqlens_q.data_ptr(),
+                           seq_lens.data_ptr(), s.cuda_stream),
+        "pattn_write_kv",
+    )
 
 
 def debug_plan(problem: Problem, cu_seqlens_q: torch.Tensor, seq_lens: torch.Tensor) -> torch.Tensor:

@@ -122,6 +122,11 @@ CONFIGS: Dict[str, Workload] = {
         "c5_mixed70b", tuple([(0, 2048)] * 32 + [(4096, 1)] * 224), 64, 8, 128, 16, "bf16"
     ),
 }
+# Phase-attribution workloads (not BASELINE configs): each half of config 3 on its own.
+ATTRIBUTION: Dict[str, Workload] = {
+    "c3p_prefill_part": CONFIGS["c3_mixed8b"].with_seqs([(0, 2048)] * 8, name="c3p_prefill_part"),
+    "c3d_decode_part": CONFIGS["c3_mixed8b"].with_seqs([(4096, 1)] * 56, name="c3d_decode_part"),
+}
 
 
 # ----------------------------------------------------------------------------
