@@ -314,6 +314,8 @@ def main():
         torch.cuda.synchronize()
     barrier()
     ms = t0.elapsed_time(t1) / K
+    # K1's SM share in the timed steps (K5's two-stream partition; all SMs when serial)
+    prefill_sms_timed = pattn.last_prefill_sms(local)
     # per-kernel average durations (only kinds that were launched)
     kern_ms = {}
     for k in range(NK):
@@ -413,15 +415,22 @@ def main():
 
     peaks = load_peaks()
     work = kernel_work(w)
+    num_sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    prefill_sms = prefill_sms_timed if pre_sms_known(kmask, pattn) else num_sms
+    sm_share = min(1.0, prefill_sms / num_sms)
     rl = {}
     pre_name = "prefill" if "prefill" in kern_ms else ("generic" if "generic" in kern_ms else None)
     traffic = load_traffic(args.workload)
     if pre_name and work["prefill_flops"] > 0:
         t = kern_ms[pre_name] * 1e-3
         a = work["prefill_flops"] / t / 1e12
-        rl["prefill"] = {"bound": "tensor", "achieved": a, "peak": peaks["bf16"], "unit": "TFLOP/s",
-                         "frac": a / peaks["bf16"], "traffic": traffic.get(pre_name), "kernel": pre_name,
-                         "kernel_ms": kern_ms[pre_name], "share_of_step": kern_ms[pre_name] / ms}
+        # two streams: K1 runs on the P SMs K5 gave it (the decode kernel has the rest), so its
+        # tensor roof is the measured peak x P / #SMs; serial: P = all SMs
+        pk = peaks["bf16"] * sm_share
+        rl["prefill"] = {"bound": "tensor", "achieved": a, "peak": pk, "unit": "TFLOP/s",
+                         "frac": a / pk, "traffic": traffic.get(pre_name), "kernel": pre_name,
+                         "kernel_ms": kern_ms[pre_name], "share_of_step": kern_ms[pre_name] / ms,
+                         "prefill_sms": prefill_sms, "num_sms": num_sms}
     if "decode" in kern_ms and work["decode_bytes"] > 0:
         t = kern_ms["decode"] * 1e-3
         a = work["decode_bytes"] / t / 1e9
@@ -482,6 +491,10 @@ def main():
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def pre_sms_known(kmask, pattn):
+    return bool(kmask & (1 << pattn.KERNEL_PREFILL))
 
 
 def local_workload(w, mode, world, rank):

@@ -205,6 +205,48 @@ PATTN_API pattn_status_t pattn_write_kv(const pattn_problem_t* p, const void* k_
                                         void* v_cache, const int32_t* block_table, const int32_t* cu_seqlens_q,
                                         const int32_t* seq_lens, void* stream);
 
+/*
+ * Tuning heuristics (the paper's two-step flow, §4.2: micro-benchmark sweeps
+ * outside the runtime, results "export[ed] as heuristics --- simple if-else decision
+ * trees" that also cover scenarios not in the sweep).  A tree maps host-known batch
+ * features to the planner's launch knobs (H1); libpattn consults it in every call.
+ * Precedence: PATTN_* environment overrides > the loaded tree > built-in defaults.
+ */
+typedef struct pattn_tuning {
+  int32_t items_per_sm;       /* decode: target (segment x KV head x head group) work items per SM (default 16) */
+  int32_t min_chunk_tokens;   /* decode: shortest split segment, in keys (default 256) */
+  int32_t decode_ctas_per_sm; /* decode: resident K2 CTAs per SM, 1..4 (default 2) */
+} pattn_tuning_t;           /* 0 in a field = built-in default */
+
+enum {
+  PATTN_FEAT_NUM_SEQS = 0,      /* num_seqs */
+  PATTN_FEAT_NUM_TOKENS = 1,    /* num_tokens */
+  PATTN_FEAT_MAX_QUERY_LEN = 2, /* max_query_len hint (<= 0: num_tokens) -- 1 means a decode-only batch */
+  PATTN_FEAT_MAX_SEQ_LEN = 3,   /* max_seq_len hint (<= 0: max_blocks_per_seq * block_size) */
+  PATTN_FEAT_COUNT = 4
+};
+
+/* One node of a decision tree, stored as an array with the root at index 0.
+ * Internal node: feature in [0, PATTN_FEAT_COUNT), children lt / ge with index > this
+ * node's (so every tree is finite and acyclic): value < threshold -> lt, else ge.
+ * Leaf: feature = -1; `leaf` holds the knobs. */
+typedef struct pattn_tree_node {
+  int32_t feature;
+  int32_t lt, ge;
+  double threshold;
+  pattn_tuning_t leaf;
+} pattn_tree_node_t;
+
+/* Install (copy) a tree for all later calls in this process; nodes == NULL or n_nodes == 0
+ * removes it.  A malformed tree (bad feature, child index <= parent or >= n_nodes, leaf
+ * knobs out of range) returns PATTN_ERR_INVALID_ARG and leaves the current tree in place.
+ * Thread-safe; not meant to be called concurrently with in-flight planning of other threads. */
+PATTN_API pattn_status_t pattn_set_tuning_tree(const pattn_tree_node_t* nodes, int32_t n_nodes);
+
+/* Host-only: the knobs the planner will use for problem p (tree leaf, env overrides and
+ * defaults resolved), written to *out.  No device work. */
+PATTN_API pattn_status_t pattn_plan_tuning(const pattn_problem_t* p, pattn_tuning_t* out);
+
 /* Static string for a status code. */
 PATTN_API const char* pattn_status_string(pattn_status_t s);
 

@@ -394,10 +394,10 @@ int env_or(const char* name, int dflt) {
 // Launch shape: one or two CTAs per SM, each with 1 producer + NCW consumer warps and an
 // NST-stage ring; ~160 KB of K/V in flight per SM.  Env overrides for sweeps:
 // PATTN_DECODE_WARPS (4|8), PATTN_DECODE_CTAS (1|2), PATTN_DECODE_RING_KB.
-DecodeLaunch plan_decode(const Params& p, int num_sms, size_t max_smem) {
+DecodeLaunch plan_decode(const Params& p, int num_sms, size_t max_smem, int ctas_per_sm) {
   DecodeLaunch dl;
   dl.consumer_warps = env_or("PATTN_DECODE_WARPS", 4) == 8 ? 8 : 4;
-  int ctas = env_or("PATTN_DECODE_CTAS", 2);
+  int ctas = ctas_per_sm;  // tuning tree / PATTN_DECODE_CTAS, resolved by the planner
   if (ctas < 1) ctas = 1;
   if (ctas > 4) ctas = 4;
   const size_t stage = (size_t)4 * kSub * p.D;  // K + V of one 16-key sub-block, bf16

@@ -22,7 +22,7 @@ struct DecodeLaunch {
   int consumer_warps;
   size_t smem;
 };
-DecodeLaunch plan_decode(const Params& p, int num_sms, size_t max_smem);
+DecodeLaunch plan_decode(const Params& p, int num_sms, size_t max_smem, int ctas_per_sm);
 cudaError_t launch_decode(const Params& p, const DecodeLaunch& dl, const CUtensorMap& tmK, const CUtensorMap& tmV,
                           cudaStream_t stream);
 

@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <vector>
 
 #include "kernels.h"
 #include "params.h"
@@ -78,6 +79,58 @@ pattn_status_t cuda_fail(cudaError_t e) {
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 bool aligned16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15u) == 0; }
 
+// ---- tuning tree (pattn_set_tuning_tree): copied under a mutex, read by every plan
+struct TuningTree {
+  std::mutex mu;
+  std::vector<pattn_tree_node_t> nodes;
+};
+TuningTree& tuning_tree() {
+  static TuningTree t;
+  return t;
+}
+
+bool leaf_ok(const pattn_tuning_t& t) {
+  return t.items_per_sm >= 0 && t.items_per_sm <= 4096 && t.min_chunk_tokens >= 0 && t.min_chunk_tokens <= (1 << 24) &&
+         t.decode_ctas_per_sm >= 0 && t.decode_ctas_per_sm <= 4;
+}
+
+double feature_value(const pattn_problem_t* p, int f) {
+  switch (f) {
+    case PATTN_FEAT_NUM_SEQS: return p->num_seqs;
+    case PATTN_FEAT_NUM_TOKENS: return p->num_tokens;
+    case PATTN_FEAT_MAX_QUERY_LEN: return p->max_query_len > 0 ? p->max_query_len : p->num_tokens;
+    case PATTN_FEAT_MAX_SEQ_LEN:
+      return p->max_seq_len > 0 ? p->max_seq_len : (double)p->max_blocks_per_seq * p->block_size;
+  }
+  return 0.0;
+}
+
+// Tree leaf for p (all zero when no tree is loaded), then env overrides, then defaults.
+pattn_tuning_t resolve_tuning(const pattn_problem_t* p) {
+  pattn_tuning_t t{0, 0, 0};
+  {
+    TuningTree& tt = tuning_tree();
+    std::lock_guard<std::mutex> g(tt.mu);
+    if (!tt.nodes.empty()) {
+      int i = 0;
+      while (tt.nodes[i].feature >= 0) {
+        const pattn_tree_node_t& n = tt.nodes[i];
+        i = feature_value(p, n.feature) < n.threshold ? n.lt : n.ge;
+      }
+      t = tt.nodes[i].leaf;
+    }
+  }
+  const char* e;
+  if ((e = getenv("PATTN_ITEMS_PER_SM")) && *e) t.items_per_sm = atoi(e);
+  if ((e = getenv("PATTN_MIN_CHUNK_TOKENS")) && *e) t.min_chunk_tokens = atoi(e);
+  if ((e = getenv("PATTN_DECODE_CTAS")) && *e) t.decode_ctas_per_sm = atoi(e);
+  if (t.items_per_sm <= 0) t.items_per_sm = 16;
+  if (t.min_chunk_tokens <= 0) t.min_chunk_tokens = 256;
+  if (t.decode_ctas_per_sm <= 0) t.decode_ctas_per_sm = 2;
+  if (t.decode_ctas_per_sm > 4) t.decode_ctas_per_sm = 4;
+  return t;
+}
+
 struct Plan {
   bool use_k1 = false, use_k2 = false, use_k4 = false;
   int block_q = 1, HG = 1, rpw = 8;
@@ -89,6 +142,7 @@ struct Plan {
   DecodeLaunch dl{};
   PrefillLaunch pl{};
   bool kv_tok_inner = false;
+  pattn_tuning_t tuning{};
 };
 
 pattn_status_t check_problem(const pattn_problem_t* p) {
@@ -144,6 +198,7 @@ pattn_status_t make_plan(const pattn_problem_t* p, const void* q, const void* kc
   pattn_status_t st = check_problem(p);
   if (st != PATTN_OK) return st;
   DeviceInfo di = device_info();
+  pl->tuning = resolve_tuning(p);
   pl->num_sms = di.ok ? di.sms : 148;
   pl->max_smem = di.ok ? di.max_smem : 227 * 1024;
   const int G = p->num_q_heads / p->num_kv_heads;
@@ -186,8 +241,9 @@ pattn_status_t make_plan(const pattn_problem_t* p, const void* q, const void* kc
     pl->target_items = pl->num_sms * 64;
     pl->min_chunk = 1;
   } else {
-    pl->target_items = env_int("PATTN_TARGET_ITEMS", pl->num_sms * 16);
-    pl->min_chunk = env_int("PATTN_MIN_CHUNK_BLOCKS", std::max(1, 256 / p->block_size));
+    pl->target_items = env_int("PATTN_TARGET_ITEMS", pl->num_sms * pl->tuning.items_per_sm);
+    pl->min_chunk = env_int("PATTN_MIN_CHUNK_BLOCKS",
+                            std::max(1, (pl->tuning.min_chunk_tokens + p->block_size - 1) / p->block_size));
   }
   if (pl->target_items < 1) pl->target_items = 1;
   if (pl->min_chunk < 1) pl->min_chunk = 1;
@@ -219,7 +275,7 @@ pattn_status_t make_plan(const pattn_problem_t* p, const void* q, const void* kc
     if (pl->k4_grid < 1) pl->k4_grid = 1;
   }
   fill_params(p, *pl, &probe);
-  if (pl->use_k2) pl->dl = plan_decode(probe, pl->num_sms, pl->max_smem);
+  if (pl->use_k2) pl->dl = plan_decode(probe, pl->num_sms, pl->max_smem, pl->tuning.decode_ctas_per_sm);
   if (pl->use_k1) pl->pl = plan_prefill(probe, pl->num_sms);
   return PATTN_OK;
 }
@@ -638,6 +694,34 @@ pattn_status_t pattn_write_kv(const pattn_problem_t* p, const void* k_new, const
   if (!di.ok) return cuda_fail(cudaGetLastError());
   const cudaError_t e = launch_write_kv(w, di.sms, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? PATTN_OK : cuda_fail(e);
+}
+
+pattn_status_t pattn_set_tuning_tree(const pattn_tree_node_t* nodes, int32_t n_nodes) {
+  std::vector<pattn_tree_node_t> v;
+  if (nodes && n_nodes > 0) {
+    for (int i = 0; i < n_nodes; ++i) {
+      const pattn_tree_node_t& n = nodes[i];
+      if (n.feature < 0) {
+        if (!leaf_ok(n.leaf)) return PATTN_ERR_INVALID_ARG;
+      } else if (n.feature >= PATTN_FEAT_COUNT || n.lt <= i || n.ge <= i || n.lt >= n_nodes || n.ge >= n_nodes ||
+                 !(n.threshold == n.threshold)) {
+        return PATTN_ERR_INVALID_ARG;
+      }
+    }
+    v.assign(nodes, nodes + n_nodes);
+  }
+  TuningTree& tt = tuning_tree();
+  std::lock_guard<std::mutex> g(tt.mu);
+  tt.nodes.swap(v);
+  return PATTN_OK;
+}
+
+pattn_status_t pattn_plan_tuning(const pattn_problem_t* p, pattn_tuning_t* out) {
+  if (!out) return PATTN_ERR_INVALID_ARG;
+  const pattn_status_t st = check_problem(p);
+  if (st != PATTN_OK) return st;
+  *out = resolve_tuning(p);
+  return PATTN_OK;
 }
 
 int32_t pattn_version(void) { return kVersion; }

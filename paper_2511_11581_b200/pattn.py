@@ -89,6 +89,8 @@ EXPORTS = [
     "pattn_last_error",
     "pattn_version",
     "pattn_write_kv",
+    "pattn_set_tuning_tree",
+    "pattn_plan_tuning",
 ]
 
 
@@ -126,9 +128,27 @@ def load() -> ctypes.CDLL:
             if hasattr(lib, "pattn_write_kv"):  # absent only in older A/B builds (PATTN_LIB)
                 lib.pattn_write_kv.restype = ctypes.c_int
                 lib.pattn_write_kv.argtypes = [P, vp, vp, ctypes.c_int64, ctypes.c_int64, vp, vp, vp, vp, vp, vp]
+            if hasattr(lib, "pattn_set_tuning_tree"):  # absent only in older A/B builds
+                lib.pattn_set_tuning_tree.restype = ctypes.c_int
+                lib.pattn_set_tuning_tree.argtypes = [vp, ctypes.c_int32]
+                lib.pattn_plan_tuning.restype = ctypes.c_int
+                lib.pattn_plan_tuning.argtypes = [P, vp]
             lib.pattn_version.restype = ctypes.c_int32
             lib.pattn_last_error.restype = ctypes.c_char_p
             _lib = lib
+            # the fitted planner heuristics (scripts/tune.py -> tuning_tree.json, §4.2)
+            tree_path = os.path.join(_HERE, "tuning_tree.json")
+            if hasattr(lib, "pattn_set_tuning_tree") and os.path.exists(tree_path) and \
+                    not os.environ.get("PATTN_NO_TUNING_TREE"):
+                import json
+
+                from . import tuner
+
+                nodes = tuner.flatten(json.load(open(tree_path)))
+                arr = (tuner.TreeNode * len(nodes))(*nodes)
+                code = lib.pattn_set_tuning_tree(arr, len(nodes))
+                if code != PATTN_OK:
+                    raise PattnError(code, f"pattn_set_tuning_tree({tree_path})")
     return _lib
 
 
@@ -394,6 +414,17 @@ def make_events(n_steps: int):
             e.record()
         out.append(evs)
     return out
+
+
+def last_prefill_sms(device=None) -> int:
+    """K1's SM count chosen by K5 in the last call that used the cached workspace (header word
+    kHdrPrefillCtas): the two-stream partition, or all SMs when serial.  Reads 4
+    bytes device->host (synchronous); for reporting only, never on the hot path."""
+    dev = torch.device("cuda", device if device is not None else torch.cuda.current_device())
+    b = _ws.buf.get(dev.index)
+    if b is None:
+        raise RuntimeError("no cached workspace on this device")
+    return int(b[28:32].view(torch.int32).item())
 
 
 def version() -> int:

@@ -12,7 +12,7 @@ for c in c2_decode8b c4_decode128k c3_mixed8b; do
       python bench.py --workload $c --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 done
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:"k1_prefill" -s 2 -c 1 -o gpurun_out/k1_c3_full -f \
-    python bench.py --workload c3_mixed8b --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_k1_full.log 2>&1
+    python bench.py --workload c3_mixed8b --streams 1 --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_k1_full.log 2>&1
 timeout 300 ncu --set full --import-source on --clock-control none -k regex:"k2_decode" -s 3 -c 1 -o gpurun_out/k2_c2_full -f \
     python bench.py --workload c2_decode8b --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_k2_full.log 2>&1
 python scripts/ncu_summary.py gpurun_out/ncu_c*.csv

@@ -88,3 +88,23 @@ def test_plan_partitions_and_balance():
     kv = shard.plan_shards(cu, sl, 64, 8, 128, 8, "kvhead")
     assert [list(r) for r in kv.kv_heads] == [[i] for i in range(8)]
     assert kv.q_heads[3] == range(24, 32)
+
+
+def test_bench_local_workloads_partition_config5():
+    # bench.py --shard: every rank's local workload is a disjoint piece of ONE global batch;
+    # config 5 at P=8 by sequence = 4 prefills + 28 decodes per rank; by KV head
+    # = 1 KV head + 8 query heads per rank over all 256 sequences
+    import bench
+    from workloads import CONFIGS
+
+    w = CONFIGS["c5_mixed70b"]
+    seqs = []
+    for r in range(8):
+        lw = bench.local_workload(w, "seq", 8, r)
+        assert sum(1 for _, q in lw.seqs if q > 1) == 4 and sum(1 for _, q in lw.seqs if q == 1) == 28
+        seqs += list(lw.seqs)
+    assert sorted(seqs) == sorted(w.seqs)
+    for r in range(8):
+        lw = bench.local_workload(w, "kvhead", 8, r)
+        assert (lw.num_kv_heads, lw.num_q_heads, lw.seqs) == (1, 8, w.seqs)
+    assert bench.local_workload(w, "none", 8, 3) is w
