@@ -91,10 +91,25 @@ constexpr uint32_t kSub16Bytes = 16 * kD * 2;  // 4 KB: one 16-key sub-block of 
 #define PATTN_K1_KST 4
 #endif
 #ifndef PATTN_K1_VST
-#define PATTN_K1_VST 5
+#define PATTN_K1_VST 4
 #endif
 constexpr int kKStages = PATTN_K1_KST;
 constexpr int kVStages = PATTN_K1_VST;  // V waits on PV (later than S), so it gets the deeper ring
+// Exponential-phase ping-pong between the two softmax warpgroups (named barriers 1, 2): the
+// halves' S tiles complete ~one UMMA apart, so without it both warpgroups hit MUFU.EX2 at the
+// same time (the pipe is saturated for ~half a tile period and idle for the rest: trace
+// "max->exp" 1276 clk of a ~2400 clk period).  With it, WG a's exponentials of tile j run
+// while WG b does its load / max / P store, and vice versa.
+#ifndef PATTN_K1_PINGPONG
+#define PATTN_K1_PINGPONG 0  // measured slower: off
+#endif
+constexpr int kBarExpA = 1, kBarExpB = 2;
+// P -> bf16 with integer ops (round half up on the fp32 bits, then a byte permute) instead of
+// F2FP: F2FP issues on the same XU pipe as MUFU.EX2 (measured 8 clk per warp instruction per
+// SMSP for both, scripts/micro/pipes.cu), i.e. one third of the softmax's XU time.
+#ifndef PATTN_K1_ALU_PACK
+#define PATTN_K1_ALU_PACK 0  // measured slower: off
+#endif  // "half a may start its exponentials" / "half b may"
 constexpr float kRescaleThreshold = 8.0f;  // log2 domain: rescale O only if the max grows by > 2^8
 #ifndef PATTN_POLY_MASK
 #define PATTN_POLY_MASK 255  // measured: FMA-pipe exp2 did not pay off here
@@ -105,7 +120,11 @@ constexpr int kPolyMask = PATTN_POLY_MASK;  // exp2 pair j on the FMA pipe iff (
 constexpr uint32_t kOffQ = 0;  // half a: [0, 32K), half b: [32K, 64K)
 constexpr uint32_t kOffK = kOffQ + 2 * kQTile;
 constexpr uint32_t kOffV = kOffK + kKStages * kTile;
-constexpr uint32_t kOffBar = kOffV + kVStages * kTile;
+// epilogue staging: per half 16 KB = 4 warps x 32 rows x 128 B (one 64-wide d half at a time),
+// 128B-swizzled as the out TMA map expects
+constexpr uint32_t kStageHalf = kHalfM * 128;
+constexpr uint32_t kOffStage = kOffV + kVStages * kTile;
+constexpr uint32_t kOffBar = kOffStage + 2 * kStageHalf;
 constexpr uint32_t kSmemBytes = kOffBar + 512 + 1024;
 static_assert(kSmemBytes <= 227 * 1024, "shared memory budget");
 
@@ -123,7 +142,7 @@ struct Bars {
   uint32_t tmem_base;
 };
 constexpr int kItemRing = 2;
-constexpr int kItemConsumers = 13;  // warps 0-3, 12 and the 8 softmax warps
+constexpr int kItemConsumers = 14;  // warps 0-3, 12, 14 and the 8 softmax warps
 
 struct Item {
   int b, kvh, q0, qlen, L, ctx, tok0, ntok, kv_end, ntiles;
@@ -228,7 +247,8 @@ PATTN_DEVICE Item next_item(Bars& bar, const ItemSlot* ring, uint32_t n, int lan
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
-    k1_prefill(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ KvHeadMaps maps, Params p) {
+    k1_prefill(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmO,
+               const __grid_constant__ KvHeadMaps maps, Params p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   Bars& bar = *reinterpret_cast<Bars*>(smem + kOffBar);
@@ -294,7 +314,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int kv = (warp == 3 || warp == 12) ? 1 : 0;
     const bool owner = warp == 0 || warp == 3;  // arms the stage barrier with the tile's byte count
     const int i_lo = owner ? 0 : kN / 32, i_hi = i_lo + kN / 32;  // 2 sub-blocks per warp
-    if (lane == 0 && kv == 0) tma_prefetch_desc(&tmQ);
     // A 128-key tile = 8 sub-blocks of 16 keys; sub-block idx is slots [(idx % n16)*16, +16)
     // of paged block bt[idx / n16] (any block size that is a multiple of 16).  One 4 KB TMA
     // box per sub-block (per-head 5-D map); the warp's 4 boxes are issued by lanes 0-3
@@ -312,15 +331,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) tma_prefetch_desc(tm);
       const int32_t* bt = p.block_table + (int64_t)x.b * p.bt_stride;
       const int nsb_valid = (x.kv_end + 15) / 16;  // sub-blocks holding visible keys
-      if (warp == 0 && lane == 0) {
-        mbar_wait(&bar.q_empty, (ic & 1u) ^ 1u);
-        mbar_arrive_expect_tx(&bar.q_full, 2 * kQTile);
-        for (int h = 0; h < 2; ++h) {
-          const int tok = x.q0 + x.tok0 + h * bq_half;
-          tma_load_4d(smem + kOffQ + h * kQTile, &tmQ, &bar.q_full, 0, 0, x.kvh, tok);
-          tma_load_4d(smem + kOffQ + h * kQTile + kHalf, &tmQ, &bar.q_full, 64, 0, x.kvh, tok);
-        }
-      }
       int id_next = id0;  // tile 0: fetched by the scheduler
       for (int jt = 0; jt < x.ntiles; ++jt) {
         const int id_cur = id_next;
@@ -476,6 +486,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) mbar_arrive(&bar.item_full[slot]);
         if (it >= n_items) break;
       }
+    } else if (warp == 14) {
+      // ================================================================ Q producer
+      // Its own warp, so that waiting for the single Q buffer to drain (the current item's
+      // last S MMA) never holds back the K/V producers' prefetch of the next item's tiles.
+      if (lane == 0) tma_prefetch_desc(&tmQ);
+      for (uint32_t ic = 0;; ++ic) {
+        const Item x = next_item(bar, ring, ic, lane);
+        if (x.ntiles < 0) break;
+        if (lane == 0) {
+          mbar_wait(&bar.q_empty, (ic & 1u) ^ 1u);
+          mbar_arrive_expect_tx(&bar.q_full, 2 * kQTile);
+          for (int h = 0; h < 2; ++h) {
+            const int tok = x.q0 + x.tok0 + h * bq_half;
+            tma_load_4d(smem + kOffQ + h * kQTile, &tmQ, &bar.q_full, 0, 0, x.kvh, tok);
+            tma_load_4d(smem + kOffQ + h * kQTile + kHalf, &tmQ, &bar.q_full, 64, 0, x.kvh, tok);
+          }
+        }
+        __syncwarp();
+      }
     }
   } else {
     // ================================================================ softmax / correction / epilogue
@@ -486,11 +515,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tS0 = tmem + kTmemS + 128 * h + lane_off;
     const uint32_t tO = tmem + kTmemO + 128 * h + lane_off;
     uint32_t tc = 0, vc = 0;  // tiles seen by this warpgroup (== PV count of this half)
-    uint32_t sc[2] = {0u, 0u};  // completed phases observed per S buffer
+    uint32_t sc0 = 0u, sc1 = 0u;  // completed phases observed per S buffer (scalars: a runtime-indexed
+                                  // array would live in local memory inside the tile loop)
     __nv_bfloat16* O = static_cast<__nv_bfloat16*>(p.out);
     const float cs = p.scale_log2;
     const float ca = fmaxf(fabsf(cs), 1e-30f);  // scale 0: -inf * 0 would be NaN; 1e-30 * s ~ 0
     uint32_t ic = 0;
+    if (PATTN_K1_PINGPONG && h == 1) named_bar_arrive(kBarExpA, 2 * kHalfM);  // half a goes first
     for (;; ++ic) {
       const Item x = next_item(bar, ring, ic, lane);
       if (x.ntiles < 0) break;
@@ -502,8 +533,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int jt = 0; jt < x.ntiles; ++jt) {
         const int sb = jt & 1;  // S buffer of this tile (P is written back over it)
         const uint32_t tS = tS0 + 64 * sb;
-        mbar_wait(&bar.s_full[h][sb], sc[sb] & 1u);
-        ++sc[sb];
+        mbar_wait(&bar.s_full[h][sb], (sb ? sc1 : sc0) & 1u);
+        sc0 += sb ? 0u : 1u;
+        sc1 += sb ? 1u : 0u;
         if (r == 0) PATTN_K1_TRACE(10 + h);
         tc_fence_after();
 #ifdef PATTN_K1_NOSOFTMAX  // timing experiment only: P = bf16 pairs of S, no max / exp / rescale
@@ -561,6 +593,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint64_t ca2 = f32x2(ca, ca), nb2 = f32x2(nbase, nbase);
         uint64_t rs2[4] = {0ull, 0ull, 0ull, 0ull};
         uint32_t pk[kN / 2];
+        // both halves see the same number of tiles per item, so the turns strictly alternate
+        if (PATTN_K1_PINGPONG) named_bar_sync(h ? kBarExpB : kBarExpA, 2 * kHalfM);
 #pragma unroll
         for (int c = 0; c < kN; c += 2) {
           // e^{scale*qk - m} in the log2 domain
@@ -577,8 +611,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             ee = f32x2(e0, e1);
           }
           rs2[(c >> 1) & 3] = fadd2(rs2[(c >> 1) & 3], ee);
-          pk[c >> 1] = pack_bf16(e0, e1);
+#if PATTN_K1_ALU_PACK
+          pk[c >> 1] = pack_bf16_alu(e0, e1);  // ALU pipe: keeps the XU pipe for MUFU.EX2
+#else
+          pk[c >> 1] = pack_bf16(e0, e1);  // F2FP: shares the XU pipe with MUFU.EX2
+#endif
         }
+        if (PATTN_K1_PINGPONG) named_bar_arrive(h ? kBarExpA : kBarExpB, 2 * kHalfM);
         const uint64_t r01 = fadd2(rs2[0], rs2[1]), r23 = fadd2(rs2[2], rs2[3]), rr = fadd2(r01, r23);
         const float rs = f32x2_lo(rr) + f32x2_hi(rr);
         if (r == 0) PATTN_K1_TRACE(34 + h);
@@ -643,7 +682,42 @@ __global__ void __launch_bounds__(kThreads, 1)
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(&bar.o_empty[h]);
-      if (row_valid) {
+      // Full 8-token slices of a warp (32 rows, all valid) leave through a TMA store from a
+      // 128B-swizzled staging slice: 8 STS.128 per thread and pass instead of 16 STG.128 that
+      // each touch 32 different 128-B lines (rows are 256 B apart in `out`) -- those flooded
+      // the MIO queue for ~4k clk per item and stalled the MMA warp's next S issue (trace).
+      const int tk_last = h * bq_half + ((r | 31) / G);  // token of the warp's last row
+      if (p.k1_tma_store && tk_last < x.ntok) {
+        uint8_t* stg = smem + kOffStage + h * kStageHalf + (warp & 3) * 4096;
+        const uint32_t row_off = (uint32_t)(r & 31) * 128;
+        const uint64_t inv2 = f32x2(inv, inv);
+        const int tok_w = x.q0 + x.tok0 + h * bq_half + (r & ~31) / G;
+#pragma unroll
+        for (int pass = 0; pass < 2; ++pass) {
+          if (lane == 0) bulk_wait_group_read0();  // the slice's previous store has read it
+          __syncwarp();
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const int c0 = pass * 64 + c * 8;
+            uint4 v;
+            uint64_t a = fmul2((uint64_t)o[c0 + 0] | ((uint64_t)o[c0 + 1] << 32), inv2);
+            v.x = pack_bf16(f32x2_lo(a), f32x2_hi(a));
+            a = fmul2((uint64_t)o[c0 + 2] | ((uint64_t)o[c0 + 3] << 32), inv2);
+            v.y = pack_bf16(f32x2_lo(a), f32x2_hi(a));
+            a = fmul2((uint64_t)o[c0 + 4] | ((uint64_t)o[c0 + 5] << 32), inv2);
+            v.z = pack_bf16(f32x2_lo(a), f32x2_hi(a));
+            a = fmul2((uint64_t)o[c0 + 6] | ((uint64_t)o[c0 + 7] << 32), inv2);
+            v.w = pack_bf16(f32x2_lo(a), f32x2_hi(a));
+            *reinterpret_cast<uint4*>(stg + row_off + ((c ^ (r & 7)) << 4)) = v;
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_4d(&tmO, stg, pass * 64, 0, x.kvh, tok_w);
+            bulk_commit_group();
+          }
+        }
+      } else if (row_valid) {
         const uint64_t inv2 = f32x2(inv, inv);
 #pragma unroll
         for (int c = 0; c < kD; c += 8) {
@@ -661,6 +735,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (r == 0) PATTN_K1_TRACE(44 + h);
     }
+    if (lane == 0) bulk_wait_group0();  // epilogue stores complete before the CTA retires
+    // drain half b's last hand-over (its final arrive on kBarExpA has no partner otherwise)
+    if (PATTN_K1_PINGPONG && h == 0) named_bar_sync(kBarExpA, 2 * kHalfM);
     if (threadIdx.x == 128) PATTN_CTA_END(k1, ic);
   }
 
@@ -689,11 +766,11 @@ PrefillLaunch plan_prefill(const Params& p, int num_sms) {
   return pl;
 }
 
-cudaError_t launch_prefill(const Params& p, const PrefillLaunch& pl, const CUtensorMap& tmQ, const KvHeadMaps& kv,
-                           cudaStream_t stream) {
+cudaError_t launch_prefill(const Params& p, const PrefillLaunch& pl, const CUtensorMap& tmQ, const CUtensorMap& tmO,
+                           const KvHeadMaps& kv, cudaStream_t stream) {
   cudaError_t e = cudaFuncSetAttribute(k1_prefill, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
   if (e != cudaSuccess) return e;
-  k1_prefill<<<pl.grid, kThreads, pl.smem, stream>>>(tmQ, kv, p);
+  k1_prefill<<<pl.grid, kThreads, pl.smem, stream>>>(tmQ, tmO, kv, p);
   return cudaGetLastError();
 }
 

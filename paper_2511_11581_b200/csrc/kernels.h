@@ -45,8 +45,8 @@ struct PrefillLaunch {
 bool prefill_supported(const Params& p);
 int prefill_block_q(int G);  // tokens per K1 Q block (BLOCK_M / G)
 PrefillLaunch plan_prefill(const Params& p, int num_sms);
-cudaError_t launch_prefill(const Params& p, const PrefillLaunch& pl, const CUtensorMap& tmQ, const KvHeadMaps& kv,
-                           cudaStream_t stream);
+cudaError_t launch_prefill(const Params& p, const PrefillLaunch& pl, const CUtensorMap& tmQ, const CUtensorMap& tmO,
+                           const KvHeadMaps& kv, cudaStream_t stream);
 
 // K6: paged KV write (reshape-and-cache).  Strides in BYTES; every row start and row_bytes
 // are multiples of 16 (checked by the API).

@@ -53,6 +53,7 @@ struct Params {
   int64_t kv_st_blk, kv_st_tok, kv_st_head;
   int64_t bt_stride;
   int64_t o_st_tok, o_st_head;
+  int32_t k1_tma_store;  // K1 epilogue: 1 -> full 8-token warp slices leave through a TMA store (tmO valid)
   float scale;       // softmax scale (Eq. 1)
   float scale_log2;  // scale * log2(e)
   // workspace

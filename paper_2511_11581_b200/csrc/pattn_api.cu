@@ -372,6 +372,24 @@ bool encode_q_map(CUtensorMap* tm, const pattn_problem_t* p, const void* q, int 
   return r == CUDA_SUCCESS;
 }
 
+// out viewed like Q, [T][Hkv][G][D]: box {64 d, G heads, 1, 32/G tokens} = the 32 rows of one
+// K1 epilogue warp (one 64-wide d half per store).  Needs 32 % G == 0.
+bool encode_o_map(CUtensorMap* tm, const pattn_problem_t* p, void* out) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  const int G = p->num_q_heads / p->num_kv_heads;
+  if (G > 32 || 32 % G != 0) return false;
+  cuuint64_t dims[4] = {(cuuint64_t)p->head_dim, (cuuint64_t)G, (cuuint64_t)p->num_kv_heads,
+                        (cuuint64_t)std::max(1, p->num_tokens)};
+  cuuint64_t strides[3] = {(cuuint64_t)p->o_stride_head * 2, (cuuint64_t)p->o_stride_head * 2 * G,
+                           (cuuint64_t)p->o_stride_tok * 2};
+  cuuint32_t box[4] = {64, (cuuint32_t)G, 1, (cuuint32_t)(32 / G)};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, out, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 struct EventRec {
   const pattn_exec_opts_t* o;
   void rec(int idx, cudaStream_t s) const {
@@ -414,7 +432,8 @@ pattn_status_t run(const pattn_problem_t* p, const void* q, const void* k_cache,
   k.part_l = reinterpret_cast<float*>(ws + pl.off_pl);
   k.part_acc = reinterpret_cast<float*>(ws + pl.off_pacc);
 
-  CUtensorMap tmQ, tmK5, tmV5;
+  CUtensorMap tmQ, tmO, tmK5, tmV5;
+  memset(&tmO, 0, sizeof(tmO));
   static thread_local KvHeadMaps head_maps;  // 16 KB: kept off the stack
   if (!metadata_only) {
     if (pl.use_k2) {
@@ -425,6 +444,7 @@ pattn_status_t run(const pattn_problem_t* p, const void* q, const void* k_cache,
     }
     if (pl.use_k1) {
       if (!encode_q_map(&tmQ, p, q, pl.block_q)) return PATTN_ERR_UNSUPPORTED;
+      k.k1_tma_store = (!getenv("PATTN_K1_NO_TMA_STORE") && encode_o_map(&tmO, p, out)) ? 1 : 0;
     }
   }
 
@@ -461,7 +481,7 @@ pattn_status_t run(const pattn_problem_t* p, const void* q, const void* k_cache,
   // the prefill CTAs release when they finish.
   if (pl.use_k1) {
     ev.rec(2 * PATTN_KERNEL_PREFILL, s1);
-    e = launch_prefill(k, pl.pl, tmQ, head_maps, s1);
+    e = launch_prefill(k, pl.pl, tmQ, tmO, head_maps, s1);
     ev.rec(2 * PATTN_KERNEL_PREFILL + 1, s1);
     if (e != cudaSuccess) return cuda_fail(e);
   }

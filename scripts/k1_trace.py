@@ -42,6 +42,13 @@ names = {1: "K_ready", 2: "V_ready", 3: "Pa_ready", 4: "Pb_ready", 5: "PVa_issue
 print("events", n)
 for t, c in ev[:160]:
     print(f"{int(t - t0):8d}  {names.get(int(c), c)}")
+# a window around the 6th item start (steady state)
+starts = np.nonzero(ev[:, 1] == 40)[0]
+if len(starts) > 6:
+    i0 = starts[5]
+    print("---- window around item 6")
+    for t, c in ev[max(0, i0 - 60): i0 + 60]:
+        print(f"{int(t - t0):8d}  {names.get(int(c), c)}")
 # per-event-type mean intervals
 for c in sorted(set(ev[:, 1].tolist())):
     ts = ev[ev[:, 1] == c, 0].astype(np.int64)
