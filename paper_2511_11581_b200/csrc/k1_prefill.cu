@@ -122,7 +122,11 @@ constexpr uint32_t kOffK = kOffQ + 2 * kQTile;
 constexpr uint32_t kOffV = kOffK + kKStages * kTile;
 // epilogue staging: per half 16 KB = 4 warps x 32 rows x 128 B (one 64-wide d half at a time),
 // 128B-swizzled as the out TMA map expects
-constexpr uint32_t kStageHalf = kHalfM * 128;
+#ifndef PATTN_K1_STAGE_FULL
+#define PATTN_K1_STAGE_FULL 0  // 1: 8 KB per warp (both d halves at once, no read wait in between)
+#endif
+constexpr uint32_t kStageWarp = PATTN_K1_STAGE_FULL ? 8192 : 4096;
+constexpr uint32_t kStageHalf = 4 * kStageWarp;
 constexpr uint32_t kOffStage = kOffV + kVStages * kTile;
 constexpr uint32_t kOffBar = kOffStage + 2 * kStageHalf;
 constexpr uint32_t kSmemBytes = kOffBar + 512 + 1024;
@@ -688,14 +692,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       // the MIO queue for ~4k clk per item and stalled the MMA warp's next S issue (trace).
       const int tk_last = h * bq_half + ((r | 31) / G);  // token of the warp's last row
       if (p.k1_tma_store && tk_last < x.ntok) {
-        uint8_t* stg = smem + kOffStage + h * kStageHalf + (warp & 3) * 4096;
+        uint8_t* stg0 = smem + kOffStage + h * kStageHalf + (warp & 3) * kStageWarp;
         const uint32_t row_off = (uint32_t)(r & 31) * 128;
         const uint64_t inv2 = f32x2(inv, inv);
         const int tok_w = x.q0 + x.tok0 + h * bq_half + (r & ~31) / G;
 #pragma unroll
         for (int pass = 0; pass < 2; ++pass) {
-          if (lane == 0) bulk_wait_group_read0();  // the slice's previous store has read it
-          __syncwarp();
+          uint8_t* stg = stg0 + (PATTN_K1_STAGE_FULL ? pass * 4096 : 0);
+          if (pass == 0 || !PATTN_K1_STAGE_FULL) {
+            if (lane == 0) bulk_wait_group_read0();  // the slice's previous store has read it
+            __syncwarp();
+          }
 #pragma unroll
           for (int c = 0; c < 8; ++c) {
             const int c0 = pass * 64 + c * 8;
