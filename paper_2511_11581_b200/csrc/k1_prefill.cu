@@ -43,7 +43,7 @@ __device__ unsigned long long g_k1_trace[5][2 * 2048];
 __device__ unsigned int g_k1_trace_n[5];
 #define PATTN_K1_TRACE_ROLE(role, cnt, code)                          \
   do {                                                                \
-    if (blockIdx.x == 0 && (cnt) < 2048) {                            \
+    if (blockIdx.x == 0 && (role) >= 0 && (cnt) < 2048) {             \
       g_k1_trace[role][2 * (cnt)] = clock64();                        \
       g_k1_trace[role][2 * (cnt) + 1] = (code);                       \
       g_k1_trace_n[role] = ++(cnt);                                   \
@@ -146,7 +146,13 @@ struct Bars {
   uint32_t tmem_base;
 };
 constexpr int kItemRing = 2;
-constexpr int kItemConsumers = 14;  // warps 0-3, 12, 14 and the 8 softmax warps
+// One MMA-issuing warp per half (warp 1: half a, warp 15: half b) so that one half's chain
+// S(j) -> softmax(j) -> PV(j) never waits behind the other half's softmax.
+#ifndef PATTN_K1_SPLIT_MMA
+#define PATTN_K1_SPLIT_MMA 1
+#endif
+constexpr int kMmaWarps = PATTN_K1_SPLIT_MMA ? 2 : 1;
+constexpr int kItemConsumers = 14 + (kMmaWarps - 1);  // warps 0-3, 12, 14, (15) and the 8 softmax warps
 
 struct Item {
   int b, kvh, q0, qlen, L, ctx, tok0, ntok, kv_end, ntiles;
@@ -263,20 +269,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   // two-stream SM partition (K5's choice): surplus CTAs leave their SM to the decode kernel
   if (p.partition && (int)blockIdx.x >= p.hdr[kHdrPrefillCtas]) return;
 #ifdef PATTN_TRACE
-  const int trace_role = warp == 1 ? 0 : warp == 0 ? 3 : warp == 3 ? 4 : warp == 4 ? 1 : 2;
+  const int trace_role = warp == 15 ? -1 : warp == 1 ? 0 : warp == 0 ? 3 : warp == 3 ? 4 : warp == 4 ? 1 : 2;
   unsigned int trace_cnt = 0;
 #endif
 
   if (threadIdx.x == 0) {
     mbar_init(&bar.q_full, 1);
-    mbar_init(&bar.q_empty, 1);
+    mbar_init(&bar.q_empty, kMmaWarps);
     for (int s = 0; s < kKStages; ++s) {
       mbar_init(&bar.k_full[s], 1);
-      mbar_init(&bar.k_empty[s], 1);
+      mbar_init(&bar.k_empty[s], kMmaWarps);
     }
     for (int s = 0; s < kVStages; ++s) {
       mbar_init(&bar.v_full[s], 1);
-      mbar_init(&bar.v_empty[s], 1);
+      mbar_init(&bar.v_empty[s], kMmaWarps);
     }
     for (int h = 0; h < 2; ++h) {
       mbar_init(&bar.s_full[h][0], 1);
@@ -362,11 +368,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         ++cnt;
       }
     }
-  } else if (warp == 1) {
-    // ================================================================ MMA issuer
+  } else if (warp == 1 || (PATTN_K1_SPLIT_MMA && warp == 15)) {
+    // ================================================================ MMA issuer(s)
     // The whole warp runs the schedule (waits, descriptor arithmetic stay warp-uniform, in
-    // uniform registers); one elected lane issues each tcgen05.mma / commit.
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
+    // uniform registers); one elected lane issues each tcgen05.mma / commit.  With two MMA
+    // warps, warp 1 issues half a's S and PV and warp 15 half b's; K / V / Q stages are
+    // released when both have committed (the empty barriers count kMmaWarps arrivals).
+    if (warp == 1)
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
+    else
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");  // warpgroup 3
+    const int h_lo = (PATTN_K1_SPLIT_MMA && warp == 15) ? 1 : 0;
+    const int h_hi = PATTN_K1_SPLIT_MMA ? h_lo + 1 : 2;
     constexpr uint32_t idS = idesc_bf16_f32(kHalfM, kN, 0, 0);   // Q (K-major) x K (K-major)
     constexpr uint32_t idPV = idesc_bf16_f32(kHalfM, kD, 0, 1);  // P (TMEM, K-major) x V (MN-major)
     // smem descriptors: start-address field = addr >> 4, so desc(base + off) = desc(base) + (off >> 4)
@@ -375,7 +388,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint64_t dV = smem_desc_sw128(sbase + kOffV, 1024, 2048);   // d halves 1 KB apart
     const bool leader = elect_one();
     uint32_t ic = 0, kc = 0, vc = 0;
-    uint32_t pc[2] = {0u, 0u};
+    uint32_t pcnt = 0u;  // PV iterations issued (the same count for every half this warp serves)
     for (;; ++ic) {
       const Item x = next_item(bar, ring, ic, lane);
       if (x.ntiles < 0) break;
@@ -395,8 +408,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (leader) PATTN_K1_TRACE(1);
           tc_fence_after();
           if (leader) {
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
+            for (int h = h_lo; h < h_hi; ++h) {
               const uint32_t tS = tmem + kTmemS + 128 * h + 64 * (jt & 1);
               const uint64_t dq = dQ + ((h * kQTile) >> 4), dk = dK + ((ks * kTile) >> 4);
 #pragma unroll
@@ -420,10 +432,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t vs = vc % kVStages;
           mbar_wait(&bar.v_full[vs], (vc / kVStages) & 1u);
           if (leader) PATTN_K1_TRACE(2);
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
+          for (int h = h_lo; h < h_hi; ++h) {
             const uint32_t tP = tmem + kTmemS + 128 * h + 64 * ((jt - 1) & 1), tO = tmem + kTmemO + 128 * h;
-            mbar_wait(&bar.p_full[h], pc[h] & 1u);
+            mbar_wait(&bar.p_full[h], pcnt & 1u);
             if (jt == 1) mbar_wait(&bar.o_empty[h], (ic & 1u) ^ 1u);
             tc_fence_after();
             if (leader) {
@@ -439,8 +450,8 @@ __global__ void __launch_bounds__(kThreads, 1)
               tc_commit(&bar.pv_done[h]);
             }
             __syncwarp();
-            ++pc[h];
           }
+          ++pcnt;
           if (leader) tc_commit(&bar.v_empty[vs]);
           __syncwarp();
           ++vc;
@@ -448,7 +459,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp >= 13) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");  // warpgroup 3
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");  // warpgroup 3 (13, 14)
     if (warp == 13) {
       // ================================================================ item scheduler
       const int n16 = p.bs / 16;
@@ -647,8 +658,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         m_run = m_use;
         // P (bf16, 2 per column) over the first 32 columns of the S buffer: the A operand of PV_h
         PATTN_TMEM_ST32(tS + 0, (pk + 0));
-        // WG a: zero V rows of slots >= L inside the last fetched sub-block (they may hold NaN)
-        if (h == 0) {
+        // Zero V rows of slots >= L inside the last fetched sub-block (they may hold NaN).  With
+        // one MMA warp, WG a does it (PV_b is issued after PV_a); with one MMA warp per half
+        // each WG does it before releasing its own P (both write the same zeros).
+        if (h == 0 || PATTN_K1_SPLIT_MMA) {
           const int z0 = x.L - key0, z1 = min(kN, nsb_valid * 16 - key0);
           if (z0 < z1 && z0 < kN) {
             const uint32_t s2 = vc % kVStages;
