@@ -152,6 +152,9 @@ constexpr int kItemRing = 2;
 #define PATTN_K1_SPLIT_MMA 1
 #endif
 constexpr int kMmaWarps = PATTN_K1_SPLIT_MMA ? 2 : 1;
+#ifndef PATTN_K1_SKEW_CLK
+#define PATTN_K1_SKEW_CLK 0
+#endif
 constexpr int kItemConsumers = 14 + (kMmaWarps - 1);  // warps 0-3, 12, 14, (15) and the 8 softmax warps
 
 struct Item {
@@ -394,6 +397,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (x.ntiles < 0) break;
       if (leader) PATTN_K1_TRACE(40);
       mbar_wait(&bar.q_full, ic & 1u);
+#if PATTN_K1_SKEW_CLK > 0
+      if (h_lo == 1) {  // experiment: start half b's chain late so the halves' exp phases interleave
+        const long long t_end = clock64() + PATTN_K1_SKEW_CLK;
+        while (clock64() < t_end) {
+        }
+      }
+#endif
       if (leader) PATTN_K1_TRACE(41);
       tc_fence_after();
       // Iteration jt: S_a(jt), S_b(jt) into S buffer jt&1 of each half, then PV_a(jt-1),

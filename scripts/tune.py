@@ -42,7 +42,7 @@ def scenarios():
     return s
 
 
-GRID = [dict(zip(tuner.KNOBS, v)) for v in itertools.product([4, 8, 16, 32], [128, 256, 1024, 4096], [1, 2, 3])]
+GRID = [dict(zip(tuner.KNOBS, v)) for v in itertools.product([4, 8, 16, 32], [128, 256, 1024, 4096], [1, 2, 3, 4])]
 
 
 def features(w):
