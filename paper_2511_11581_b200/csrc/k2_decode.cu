@@ -361,6 +361,38 @@ __global__ void __launch_bounds__((NCW + kNP) * 32, 1)
         }
       }
     }
+    if (p.fuse_reduce && x.nseg > 1) {
+      // Fused segment merge (the K3 step): the CTA that completes a unit's last
+      // segment merges all its partials, in segment order (deterministic whichever CTA is
+      // last).  Release: every writer fences, then one thread counts the segment in.
+      __threadfence();
+      named_bar_sync(1, NCW * 32);
+      volatile int* s_last = reinterpret_cast<volatile int*>(scratch);  // scratch is free again
+      if (ct == 0) {
+        const int unit = x.b * p.Hkv * p.HG + x.kvh * p.HG + x.hg;
+        const int done = atomicAdd(p.seg_cnt + unit, 1);
+        __threadfence();  // acquire: the other segments' partials are visible below
+        *s_last = (done == x.nseg - 1);
+      }
+      named_bar_sync(1, NCW * 32);
+      if (*s_last) {
+        const int cfirst = __ldg(p.cu_ch + x.b);  // first segment of the sequence
+        for (int idx = ct; idx < g_eff * D; idx += NCW * 32) {
+          const int h = idx / D, d = idx - h * D;
+          float M = -INFINITY;
+          for (int s = 0; s < x.nseg; ++s) M = fmaxf(M, __ldcg(p.part_m + (int64_t)(cfirst + s) * p.Hq + head0 + h));
+          float num = 0.f, den = 0.f;
+          for (int s = 0; s < x.nseg; ++s) {
+            const int64_t row = (int64_t)(cfirst + s) * p.Hq + head0 + h;
+            const float ms = __ldcg(p.part_m + row);
+            const float w = ms == -INFINITY ? 0.f : exp2f(ms - M);
+            den = fmaf(w, __ldcg(p.part_l + row), den);
+            num = fmaf(w, __ldcg(p.part_acc + row * D + d), num);
+          }
+          O[(int64_t)x.tok * p.o_st_tok + (int64_t)(head0 + h) * p.o_st_head + d] = __float2bfloat16_rn(num / den);
+        }
+      }
+    }
     named_bar_sync(1, NCW * 32);
     if (lane == 0 && cw == 0) PATTN_EV(k2, 5, ni);
   }

@@ -145,6 +145,10 @@ __global__ void __launch_bounds__(kMaxThreads) k5_metadata(Params p) {
     carry_qb += tot.x;
     carry_ch += tot.y;
   }
+  if (p.fuse_reduce) {  // per-unit segment counters of K2's fused merge
+    const int n = B * p.Hkv * p.HG;
+    for (int i = threadIdx.x; i < n; i += nt) p.seg_cnt[i] = 0;
+  }
   if (threadIdx.x == 0) {
     p.cu_qb[B] = carry_qb;
     p.cu_ch[B] = carry_ch;

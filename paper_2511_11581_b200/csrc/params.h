@@ -63,6 +63,8 @@ struct Params {
   float* part_m;      // [max_chunks][Hq]   (log2 domain: max of scale*log2e*s)
   float* part_l;      // [max_chunks][Hq]
   float* part_acc;    // [max_chunks][Hq][D]
+  int32_t* seg_cnt;   // [B][Hkv*HG] segments finished per decode unit (fused merge; zeroed by K5)
+  int32_t fuse_reduce;  // 1: the CTA finishing a unit's last segment merges the partials (no K3)
 };
 
 }  // namespace pattn

@@ -137,7 +137,8 @@ struct Plan {
   int target_items = 0, min_chunk = 1, split_mode = 0, max_chunks = 0;
   int num_sms = 148;
   size_t max_smem = 0;
-  size_t off_hdr = 0, off_cuqb = 0, off_cuch = 0, off_pm = 0, off_pl = 0, off_pacc = 0, total = 0;
+  size_t off_hdr = 0, off_cuqb = 0, off_cuch = 0, off_pm = 0, off_pl = 0, off_pacc = 0, off_cnt = 0, total = 0;
+  bool fuse_reduce = false;
   int k4_grid = 1;
   DecodeLaunch dl{};
   PrefillLaunch pl{};
@@ -265,6 +266,12 @@ pattn_status_t make_plan(const pattn_problem_t* p, const void* q, const void* kc
   off = align256(off + rows * sizeof(float));
   pl->off_pacc = off;
   off = align256(off + rows * (size_t)D * sizeof(float));
+  // decode segment merge: the separate K3 launch (default) or fused into K2's last CTA per unit
+  // (PATTN_K3_FUSED=1; measured slower: the per-item release fences and the serial merge by
+  // one CTA cost more than K3's launch -- config 2 +14 us, config 4 +117 us)
+  pl->fuse_reduce = pl->use_k2 && getenv("PATTN_K3_FUSED") != nullptr;
+  pl->off_cnt = off;
+  if (pl->fuse_reduce) off = align256(off + (size_t)p->num_seqs * p->num_kv_heads * pl->HG * sizeof(int32_t));
   pl->total = off;
 
   // grids
@@ -431,6 +438,8 @@ pattn_status_t run(const pattn_problem_t* p, const void* q, const void* k_cache,
   k.part_m = reinterpret_cast<float*>(ws + pl.off_pm);
   k.part_l = reinterpret_cast<float*>(ws + pl.off_pl);
   k.part_acc = reinterpret_cast<float*>(ws + pl.off_pacc);
+  k.seg_cnt = reinterpret_cast<int32_t*>(ws + pl.off_cnt);
+  k.fuse_reduce = pl.fuse_reduce ? 1 : 0;
 
   CUtensorMap tmQ, tmO, tmK5, tmV5;
   memset(&tmO, 0, sizeof(tmO));
@@ -490,10 +499,12 @@ pattn_status_t run(const pattn_problem_t* p, const void* q, const void* k_cache,
     e = launch_decode(k, pl.dl, tmK5, tmV5, sd);
     ev.rec(2 * PATTN_KERNEL_DECODE + 1, sd);
     if (e != cudaSuccess) return cuda_fail(e);
-    ev.rec(2 * PATTN_KERNEL_REDUCE, sd);
-    e = launch_reduce(k, sd);
-    ev.rec(2 * PATTN_KERNEL_REDUCE + 1, sd);
-    if (e != cudaSuccess) return cuda_fail(e);
+    if (!pl.fuse_reduce) {
+      ev.rec(2 * PATTN_KERNEL_REDUCE, sd);
+      e = launch_reduce(k, sd);
+      ev.rec(2 * PATTN_KERNEL_REDUCE + 1, sd);
+      if (e != cudaSuccess) return cuda_fail(e);
+    }
   }
   if (pl.use_k4) {
     ev.rec(2 * PATTN_KERNEL_GENERIC, s1);
@@ -661,14 +672,14 @@ pattn_status_t pattn_debug_plan(const pattn_problem_t* p, const int32_t* cu_seql
 int32_t pattn_planned_launches(const pattn_problem_t* p) {
   Plan pl;
   if (make_plan(p, nullptr, nullptr, nullptr, nullptr, &pl) != PATTN_OK) return 0;
-  return 1 + (pl.use_k1 ? 1 : 0) + (pl.use_k4 ? 1 : 0) + (pl.use_k2 ? 2 : 0);
+  return 1 + (pl.use_k1 ? 1 : 0) + (pl.use_k4 ? 1 : 0) + (pl.use_k2 ? (pl.fuse_reduce ? 1 : 2) : 0);
 }
 
 int32_t pattn_planned_kernels(const pattn_problem_t* p) {
   Plan pl;
   if (make_plan(p, nullptr, nullptr, nullptr, nullptr, &pl) != PATTN_OK) return 0;
   return (1 << PATTN_KERNEL_METADATA) | (pl.use_k1 ? 1 << PATTN_KERNEL_PREFILL : 0) |
-         (pl.use_k2 ? (1 << PATTN_KERNEL_DECODE) | (1 << PATTN_KERNEL_REDUCE) : 0) |
+         (pl.use_k2 ? (1 << PATTN_KERNEL_DECODE) | (pl.fuse_reduce ? 0 : 1 << PATTN_KERNEL_REDUCE) : 0) |
          (pl.use_k4 ? 1 << PATTN_KERNEL_GENERIC : 0);
 }
 

@@ -78,7 +78,7 @@ def test_validate_metadata_host_matches_oracle_codes(lib):
     assert lib.validate_metadata_host(p, np.array([1, 16, 17], np.int32), sl, bt) == 3
 
 
-def test_workspace_and_planned_launches(lib):
+def test_workspace_and_planned_launches(lib, monkeypatch):
     so = lib.load()
     p = _problem(lib)  # fp32 -> metadata + generic
     assert so.pattn_workspace_size(ctypes.byref(p)) > 0
@@ -86,6 +86,10 @@ def test_workspace_and_planned_launches(lib):
     pb = _problem(lib, Hq=32, Hkv=8, D=128, dtype=1, T=64, B=64, nb=16448, maxb=257)
     pb.max_query_len = 1
     assert lib.planned_launches(pb) == 3  # metadata + decode + reduce
+    monkeypatch.setenv("PATTN_K3_FUSED", "1")
+    assert lib.planned_launches(pb) == 2  # metadata + decode (segment merge fused into K2)
+    assert lib.planned_kernels(pb) == (1 << lib.KERNEL_METADATA) | (1 << lib.KERNEL_DECODE)
+    monkeypatch.delenv("PATTN_K3_FUSED")
     pb.max_query_len = 2048
     assert lib.planned_launches(pb) == 4  # + the Q-block kernel
     pb.flags = lib.FLAG_FORCE_GENERIC

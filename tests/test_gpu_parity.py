@@ -318,3 +318,38 @@ def test_compute_sanitizer_memcheck_and_racecheck():
         hazards = [l for l in r.stdout.splitlines() if "RACECHECK SUMMARY" in l and " 0 hazards" not in l]
         assert not bad and not hazards, (tool, errs, bad, hazards, r.stdout[-3000:])
         assert "ok c3_mixed8b" in r.stdout, r.stdout[-2000:]
+
+
+def test_strided_out_and_q_canary():
+    """q and out as head-slices of wider tensors (token stride (Hq+2)*D): the TMA-store epilogue
+    and every other writer must honour the strides and leave the two extra heads untouched."""
+    w = Workload("strided", ((0, 200), (700, 1), (16, 48), (3000, 1)), 32, 8, 128, 16, "bf16")
+    batch = generate(w, seed=12, dist="peaked", poison=True)
+    db = DeviceBatch(batch)
+    T, Hq, D = db.q.shape
+    qw = torch.zeros((T, Hq + 2, D), dtype=torch.bfloat16, device="cuda")
+    qw[:, 1:Hq + 1] = db.q
+    ow = torch.full((T, Hq + 2, D), 777.0, dtype=torch.bfloat16, device="cuda")
+    db.q = qw[:, 1:Hq + 1]
+    o = db.run(out=ow[:, 1:Hq + 1])
+    assert torch.all(ow[:, 0] == 777.0) and torch.all(ow[:, Hq + 1] == 777.0)
+    assert_close(out_f64(o), O.batch_attention(batch), "bf16", "strided")
+
+
+@pytest.mark.parametrize("flags", [0, 0x4])
+def test_fused_segment_merge_equals_separate_reduce(flags, monkeypatch):
+    """The decode segment merge fused into K2 (last CTA of a unit merges, PATTN_K3_FUSED=1) and
+    the separate K3 launch (default) both match the oracle; many segments per unit."""
+    w = Workload("fuse", ((20000, 1), (0, 40), (3000, 1), (17, 1), (9000, 1)), 64, 8, 128, 16, "bf16")
+    batch = generate(w, seed=13, dist="peaked")
+    ref = O.batch_attention(batch)
+    db = DeviceBatch(batch)
+    sep = db.run(flags=flags).clone()
+    monkeypatch.setenv("PATTN_K3_FUSED", "1")
+    assert P.planned_kernels(P.make_problem(db.q, db.k, 8, 16, db.bt, 5)) & (1 << P.KERNEL_REDUCE) == 0
+    fused = db.run(flags=flags).clone()
+    assert_close(out_f64(fused), ref, "bf16", "fused merge")
+    assert_close(out_f64(sep), ref, "bf16", "separate K3")
+    again = db.run(flags=flags)
+    assert torch.equal(again, fused)  # deterministic whichever CTA finishes a unit last
+    monkeypatch.delenv("PATTN_K3_FUSED")
