@@ -263,10 +263,18 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # PATTN_BENCH_BACKEND=gloo: test-only oversubscription (several ranks sharing one GPU, which
+    # NCCL refuses) to exercise the multi-rank path on a 1-GPU box; never used for numbers
+    backend = os.environ.get("PATTN_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     pattn.load()
 
     w_global = CONFIGS[args.workload] if args.workload in CONFIGS else ATTRIBUTION[args.workload]
@@ -468,6 +476,7 @@ def main():
             "block_size": w.block_size,
             "tokens_per_step_per_gpu": w.num_tokens,
             "parallelism": parallelism_text(args, world, w_global, w),
+            **({"comm_backend_test_only": backend} if backend != "nccl" else {}),
             "l2": "inputs > L2 (KV cache %.2f GB/GPU), no flush" % (kc.numel() * 2 * kc.element_size() / 1e9),
             "streams": args.streams,
             "flags": args.flags,
