@@ -69,6 +69,20 @@ PATTN_DEVICE int upper_bound_minus1(const int* __restrict__ cu, int n, int idx) 
   return lo;
 }
 
+// Same result, whole warp cooperating: every probe compares 32 entries, so n <= 1024 needs
+// <= 2 dependent loads instead of log2(n) (all lanes must call it with the same arguments).
+PATTN_DEVICE int upper_bound_minus1_warp(const int* __restrict__ cu, int n, int idx, int lane) {
+  int lo = 0, hi = n;  // invariant: cu[lo] <= idx, answer in [lo, hi)
+  while (hi - lo > 1) {
+    const int step = (hi - lo + 31) / 32;
+    const int j = lo + lane * step;
+    const unsigned m = __ballot_sync(0xffffffffu, j < hi && __ldg(cu + j) <= idx);
+    lo += (31 - __clz(m)) * step;  // lane 0 (j = lo) always satisfies the invariant
+    hi = min(hi, lo + step);
+  }
+  return lo;
+}
+
 // ---------------------------------------------------------------- shared-memory addresses
 PATTN_DEVICE uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 

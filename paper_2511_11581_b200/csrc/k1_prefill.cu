@@ -130,12 +130,21 @@ constexpr uint32_t kStageWarp = PATTN_K1_STAGE_FULL ? 8192 : 4096;
 constexpr uint32_t kStageHalf = 4 * kStageWarp;
 constexpr uint32_t kOffStage = kOffV + kVStages * kTile;
 constexpr uint32_t kOffBar = kOffStage + 2 * kStageHalf;
-constexpr uint32_t kSmemBytes = kOffBar + 512 + 1024;
+constexpr uint32_t kBarBlock = 1024;  // barriers + the item ring
+constexpr uint32_t kSmemBytes = kOffBar + kBarBlock + 1024;
 static_assert(kSmemBytes <= 227 * 1024, "shared memory budget");
 
 // TMEM columns
 constexpr uint32_t kTmemS = 0;    // S buffer (half x, tile parity y) at x*128 + y*64 (P aliased on its first 32 cols)
 constexpr uint32_t kTmemO = 256;  // O_x at 256 + x*128
+
+// Item ring depth: the scheduler runs kItemRing - 1 items ahead.  Claiming an item costs a
+// global atomic plus dependent metadata / block-table loads (~3-4k clk), more than a short
+// (1-2 tile) item lasts, so a 2-deep ring exposed it at the tail of the queue.
+#ifndef PATTN_K1_ITEM_RING
+#define PATTN_K1_ITEM_RING 2  // measured: 4 -> -5%, 8 -> -10% (claiming ahead unbalances the tail)
+#endif
+constexpr int kItemRing = PATTN_K1_ITEM_RING;
 
 struct Bars {
   uint64_t q_full, q_empty;
@@ -143,10 +152,10 @@ struct Bars {
   uint64_t v_full[kVStages], v_empty[kVStages];
   uint64_t s_full[2][2], p_full[2], pv_done[2], o_empty[2];
   // dynamic work queue (see ItemSlot)
-  uint64_t item_full[2], item_empty[2];
+  uint64_t item_full[kItemRing], item_empty[kItemRing];
   uint32_t tmem_base;
 };
-constexpr int kItemRing = 2;
+
 // One MMA-issuing warp per half (warp 1: half a, warp 15: half b) so that one half's chain
 // S(j) -> softmax(j) -> PV(j) never waits behind the other half's softmax.
 #ifndef PATTN_K1_SPLIT_MMA
@@ -170,13 +179,13 @@ struct ItemSlot {
   int ids[8];  // paged block of each 16-key sub-block of KV tile 0 (num_blocks: past the end)
 };
 constexpr uint32_t kOffItems = sizeof(Bars);
-static_assert(sizeof(Bars) + kItemRing * sizeof(ItemSlot) <= 512, "barrier block");
+static_assert(sizeof(Bars) + kItemRing * sizeof(ItemSlot) <= kBarBlock, "barrier block");
 
-__device__ __forceinline__ Item prefill_item(const Params& p, int total_qb, int it) {
+__device__ __forceinline__ Item prefill_item(const Params& p, int total_qb, int it, int lane) {
   Item x;
   const int j = total_qb - 1 - it / p.Hkv;  // last Q blocks (longest key range) first
   x.kvh = it % p.Hkv;
-  x.b = upper_bound_minus1(p.cu_qb, p.B, j);  // App. B
+  x.b = upper_bound_minus1_warp(p.cu_qb, p.B, j, lane);  // App. B P:46 (warp-cooperative search)
   const int qblk = j - __ldg(p.cu_qb + x.b);
   x.q0 = __ldg(p.cu_seqlens_q + x.b);
   x.qlen = __ldg(p.cu_seqlens_q + x.b + 1) - x.q0;
@@ -484,7 +493,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         it = __shfl_sync(0xffffffffu, it, 0);
         volatile ItemSlot* e = ring + slot;
         if (it < n_items) {
-          const Item x = prefill_item(p, total_qb, it);
+          const Item x = prefill_item(p, total_qb, it, lane);
           const int nsb_valid = (x.kv_end + 15) / 16;
           const int id = (lane < 8 && lane < nsb_valid) ? __ldg(p.block_table + (int64_t)x.b * p.bt_stride + lane / n16)
                                                         : p.num_blocks;
