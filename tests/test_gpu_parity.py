@@ -63,6 +63,9 @@ CASES = [
     ((32, 8), 128, 16, "f32", "NHD", "peaked"),
     ((16, 1), 64, 5, "f32", "HND", "uniform"),
     ((128, 2), 128, 16, "bf16", "NHD", "peaked"),  # G = 64
+    ((32, 8), 128, 80, "bf16", "NHD", "peaked"),   # bs 80 on the tcgen05 prefill path (G = 4)
+    ((64, 8), 128, 48, "bf16", "HND", "peaked"),   # bs 48: 3 sub-blocks per paged block, G = 8
+    ((8, 8), 128, 128, "bf16", "NHD", "peaked"),   # bs 128, G = 1 (BLOCK_Q = 256 tokens)
 ]
 
 
