@@ -85,7 +85,11 @@ __device__ __forceinline__ Item decode_item(const Params& p, int it) {
   return x;
 }
 
-template <int D, int NCW>
+// PIPE: each consumer warp computes the scores S^T of its NEXT sub-block (j + NCW) before the
+// softmax and P.V of the current one, so the 8-deep dependent mma chain of QK^T overlaps the
+// current sub-block's shuffles, exponentials and PV mmas (needs nst >= 2 * NCW: the warp holds
+// two stages at once).
+template <int D, int NCW, bool PIPE>
 __global__ void __launch_bounds__((NCW + kNP) * 32, 1)
     k2_decode(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, Params p,
               int nst) {
@@ -231,12 +235,40 @@ __global__ void __launch_bounds__((NCW + kNP) * 32, 1)
     // complete out of order: a waiter must have observed phase u-1 of a stage before it
     // waits on phase u, otherwise the parity test aliases and returns early.)  Items start
     // at g % NCW == 0 (the producer pads with empty stages), so warp cw takes j = cw mod NCW.
+    // S^T[16 keys x 8 heads] = K . Q^T of sub-block jj (waits for its stage)
+    auto scores = [&](int jj, float (&sc)[4]) {
+      const uint32_t gq = g + jj;
+      const uint32_t sq = gq % nst;
+      if (lane == 0) PATTN_EV(k2, 1, gq);
+      mbar_wait_tag(&full[sq], (gq / nst) & 1u, (int)gq, it, jj);
+      if (lane == 0) PATTN_EV(k2, 2, gq);
+      const uint32_t kq = ring_u32 + sq * S::kStageBytes;
+      sc[0] = sc[1] = sc[2] = sc[3] = 0.f;
+#pragma unroll
+      for (int kc = 0; kc < S::kKC; ++kc) {
+        const int key = (mat & 1) * 8 + mrow;
+        const int dd = kc * 16 + (mat >> 1) * 8;
+        const uint32_t addr = kq + (dd >> 6) * S::kHalfBytes + key * 128 + ((((dd & 63) >> 3) ^ (key & 7)) << 4);
+        uint32_t a0, a1, a2, a3;
+        ldmatrix_x4(addr, a0, a1, a2, a3);
+        mma_bf16_16816(sc, a0, a1, a2, a3, bq[kc][0], bq[kc][1]);
+      }
+    };
+    float sc_next[4] = {0.f, 0.f, 0.f, 0.f};
+    if (PIPE && cw < nsb) scores(cw, sc_next);
     for (int j = cw; j < nsb; j += NCW) {
       const uint32_t gg = g + j;
       const uint32_t s = gg % nst;
-      if (lane == 0) PATTN_EV(k2, 1, gg);
-      mbar_wait_tag(&full[s], (gg / nst) & 1u, (int)gg, it, j);
-      if (lane == 0) PATTN_EV(k2, 2, gg);
+      float sc[4];
+      if (PIPE) {
+        sc[0] = sc_next[0];
+        sc[1] = sc_next[1];
+        sc[2] = sc_next[2];
+        sc[3] = sc_next[3];
+        if (j + NCW < nsb) scores(j + NCW, sc_next);  // overlaps this sub-block's softmax / PV
+      } else {
+        scores(j, sc);
+      }
       const uint32_t kst = ring_u32 + s * S::kStageBytes;
       const uint32_t vst = kst + S::kOpBytes;
       const int valid = x.L - (x.sb0 + j) * kSub;  // slots [0, valid) hold real keys
@@ -252,16 +284,6 @@ __global__ void __launch_bounds__((NCW + kNP) * 32, 1)
           *reinterpret_cast<uint4*>(vgen + h * S::kHalfBytes + row * 128 + ch * 16) = make_uint4(0, 0, 0, 0);
         }
         __syncwarp();
-      }
-      float sc[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-      for (int kc = 0; kc < S::kKC; ++kc) {
-        const int key = (mat & 1) * 8 + mrow;
-        const int dd = kc * 16 + (mat >> 1) * 8;
-        const uint32_t addr = kst + (dd >> 6) * S::kHalfBytes + key * 128 + ((((dd & 63) >> 3) ^ (key & 7)) << 4);
-        uint32_t a0, a1, a2, a3;
-        ldmatrix_x4(addr, a0, a1, a2, a3);
-        mma_bf16_16816(sc, a0, a1, a2, a3, bq[kc][0], bq[kc][1]);
       }
       // sc[0..1]: key r, heads 2c, 2c+1; sc[2..3]: key r + 8
       const float s0 = r < valid ? sc[0] * p.scale_log2 : -INFINITY;
@@ -399,10 +421,14 @@ __global__ void __launch_bounds__((NCW + kNP) * 32, 1)
   if (warp == 1 && lane == 0) PATTN_CTA_END(k2, ni);
 }
 
+int env_or(const char* name, int dflt);
+
 template <int D, int NCW>
 cudaError_t launch_dw(const Params& p, const DecodeLaunch& dl, const CUtensorMap& tmK, const CUtensorMap& tmV,
                       cudaStream_t stream) {
-  auto kern = k2_decode<D, NCW>;
+  // measured slower (config 2 167 -> 200 us, 36-SM decode 603 -> 993 us): opt-in only
+  const bool pipe = env_or("PATTN_K2_PIPE", 0) != 0 && dl.stages >= 2 * NCW;
+  auto kern = pipe ? k2_decode<D, NCW, true> : k2_decode<D, NCW, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dl.smem);
   if (e != cudaSuccess) return e;
   kern<<<dl.grid, (NCW + kNP) * 32, dl.smem, stream>>>(tmK, tmV, p, dl.stages);
