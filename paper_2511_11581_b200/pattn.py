@@ -365,6 +365,14 @@ def write_kv(
     )
 
 
+def hostio_workspace_size(problem: Problem) -> int:
+    """Bytes of device workspace pattn_unified_attention_hostio needs (q/out staging + metadata)."""
+    n = load().pattn_hostio_workspace_size(ctypes.byref(problem))
+    if n == 0:
+        raise PattnError(1, "pattn_hostio_workspace_size")
+    return int(n)
+
+
 def debug_plan(problem: Problem, cu_seqlens_q: torch.Tensor, seq_lens: torch.Tensor) -> torch.Tensor:
     """Run only the metadata kernel K5 and return its plan (int32 device tensor, layout in pattn.h)."""
     lib = load()
