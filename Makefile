@@ -9,7 +9,7 @@ NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC,-fvisibility=hidden
            --expt-relaxed-constexpr -Iinclude -I$(CSRC) -DPATTN_BUILD $(EXTRA)
 SRCS    := $(CSRC)/pattn_api.cu $(CSRC)/k5_metadata.cu $(CSRC)/k4_generic.cu $(CSRC)/k2_decode.cu \
            $(CSRC)/k3_reduce.cu $(CSRC)/k1_prefill.cu \
-           $(CSRC)/k6_write_kv.cu
+           $(CSRC)/k6_write_kv.cu $(CSRC)/k7_baseline.cu
 OBJS    := $(patsubst $(CSRC)/%.cu,build/%.o,$(SRCS))
 HDRS    := $(wildcard $(CSRC)/*.h $(CSRC)/*.cuh) include/pattn.h
 

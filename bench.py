@@ -455,6 +455,10 @@ def main():
         rl["decode"] = {"bound": "hbm", "achieved": a, "peak": peaks["hbm"], "unit": "GB/s",
                         "frac": a / peaks["hbm"], "traffic": traffic.get("decode"), "kernel": "decode",
                         "kernel_ms": kern_ms["decode"], "share_of_step": kern_ms["decode"] / ms}
+    if "baseline" in kern_ms:  # the paper's App. A kernel (--flags 16): SIMT, reported by time only
+        rl["baseline"] = {"bound": "alu", "achieved": work["total_flops"] / (kern_ms["baseline"] * 1e-3) / 1e12,
+                          "peak": None, "unit": "TFLOP/s", "frac": None, "traffic": None, "kernel": "baseline",
+                          "kernel_ms": kern_ms["baseline"], "share_of_step": kern_ms["baseline"] / ms}
     dominant = max(rl.values(), key=lambda r: r["kernel_ms"]) if rl else None
 
     cpu = None

@@ -110,6 +110,9 @@ typedef struct pattn_problem {
 #define PATTN_FLAG_NO_SPLIT 0x2u       /* decode: one segment per sequence (no parallel tiled softmax) */
 #define PATTN_FLAG_FORCE_SPLIT 0x4u    /* decode: always split into segments even for short sequences */
 #define PATTN_FLAG_SERIAL 0x8u         /* single stream even when a second stream is supplied */
+#define PATTN_FLAG_BASELINE 0x10u      /* the paper's baseline kernel (App. A): one warp per
+                                          (query token, query head), tile = BLOCK_SIZE keys; for
+                                          comparison only -- every row, prefill and decode */
 
 /* Kernel kinds, for pattn_exec_opts_t.events and pattn_debug_plan(). */
 enum {
@@ -118,7 +121,8 @@ enum {
   PATTN_KERNEL_DECODE = 2,   /* K2: split-KV decode, "parallel tiled softmax" */
   PATTN_KERNEL_REDUCE = 3,   /* K3: segment reduction */
   PATTN_KERNEL_GENERIC = 4,  /* K4: generic SIMT Q-block kernel (fp32 path, fallback shapes) */
-  PATTN_KERNEL_COUNT = 5
+  PATTN_KERNEL_BASELINE = 5, /* K7: the paper's baseline kernel (PATTN_FLAG_BASELINE only) */
+  PATTN_KERNEL_COUNT = 6
 };
 
 /*

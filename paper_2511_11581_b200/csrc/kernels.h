@@ -48,6 +48,9 @@ PrefillLaunch plan_prefill(const Params& p, int num_sms);
 cudaError_t launch_prefill(const Params& p, const PrefillLaunch& pl, const CUtensorMap& tmQ, const CUtensorMap& tmO,
                            const KvHeadMaps& kv, cudaStream_t stream);
 
+// K7: the paper's baseline per-(token, head) kernel (App. A), PATTN_FLAG_BASELINE only.
+cudaError_t launch_baseline(const Params& p, cudaStream_t stream);
+
 // K6: paged KV write (reshape-and-cache).  Strides in BYTES; every row start and row_bytes
 // are multiples of 16 (checked by the API).
 struct WriteKvParams {

@@ -132,7 +132,7 @@ pattn_tuning_t resolve_tuning(const pattn_problem_t* p) {
 }
 
 struct Plan {
-  bool use_k1 = false, use_k2 = false, use_k4 = false;
+  bool use_k1 = false, use_k2 = false, use_k4 = false, use_k7 = false;
   int block_q = 1, HG = 1, rpw = 8;
   int target_items = 0, min_chunk = 1, split_mode = 0, max_chunks = 0;
   int num_sms = 148;
@@ -216,10 +216,14 @@ pattn_status_t make_plan(const pattn_problem_t* p, const void* q, const void* kc
   const bool q_ok = (p->q_stride_tok % 8 == 0) && (p->q_stride_head % 8 == 0) && (q == nullptr || aligned16(q));
   const bool o_ok = (p->o_stride_tok % 8 == 0) && (p->o_stride_head % 8 == 0) && (out == nullptr || aligned16(out));
   pl->use_k2 = bf16 && !generic && p->block_size % 16 == 0 && tma_ok && q_ok && o_ok;
+  if (p->flags & PATTN_FLAG_BASELINE) {  // the paper's baseline kernel alone (comparison only)
+    pl->use_k7 = true;
+    pl->use_k2 = false;
+  }
 
   Params probe;
   fill_params(p, *pl, &probe);
-  pl->use_k1 = bf16 && !generic && tma_ok && q_ok && o_ok && prefill_supported(probe);
+  pl->use_k1 = bf16 && !generic && !pl->use_k7 && tma_ok && q_ok && o_ok && prefill_supported(probe);
   const int max_q = p->max_query_len > 0 ? p->max_query_len : p->num_tokens;
   const bool maybe_prefill = max_q > 1 || !pl->use_k2;
   if (pl->use_k1) {
@@ -227,7 +231,7 @@ pattn_status_t make_plan(const pattn_problem_t* p, const void* q, const void* kc
     pl->use_k1 = maybe_prefill;
   } else {
     pl->block_q = G <= 32 ? std::max(1, 32 / G) : 1;
-    pl->use_k4 = maybe_prefill;
+    pl->use_k4 = maybe_prefill && !pl->use_k7;
   }
   const int bm = pl->block_q * G;
   pl->rpw = bm <= 32 ? 8 : 16;
@@ -506,6 +510,12 @@ pattn_status_t run(const pattn_problem_t* p, const void* q, const void* k_cache,
       if (e != cudaSuccess) return cuda_fail(e);
     }
   }
+  if (pl.use_k7) {
+    ev.rec(2 * PATTN_KERNEL_BASELINE, s1);
+    e = launch_baseline(k, s1);
+    ev.rec(2 * PATTN_KERNEL_BASELINE + 1, s1);
+    if (e != cudaSuccess) return cuda_fail(e);
+  }
   if (pl.use_k4) {
     ev.rec(2 * PATTN_KERNEL_GENERIC, s1);
     e = launch_generic(k, pl.k4_grid, pl.rpw, s1);
@@ -672,7 +682,8 @@ pattn_status_t pattn_debug_plan(const pattn_problem_t* p, const int32_t* cu_seql
 int32_t pattn_planned_launches(const pattn_problem_t* p) {
   Plan pl;
   if (make_plan(p, nullptr, nullptr, nullptr, nullptr, &pl) != PATTN_OK) return 0;
-  return 1 + (pl.use_k1 ? 1 : 0) + (pl.use_k4 ? 1 : 0) + (pl.use_k2 ? (pl.fuse_reduce ? 1 : 2) : 0);
+  return 1 + (pl.use_k1 ? 1 : 0) + (pl.use_k4 ? 1 : 0) + (pl.use_k7 ? 1 : 0) +
+         (pl.use_k2 ? (pl.fuse_reduce ? 1 : 2) : 0);
 }
 
 int32_t pattn_planned_kernels(const pattn_problem_t* p) {
@@ -680,7 +691,7 @@ int32_t pattn_planned_kernels(const pattn_problem_t* p) {
   if (make_plan(p, nullptr, nullptr, nullptr, nullptr, &pl) != PATTN_OK) return 0;
   return (1 << PATTN_KERNEL_METADATA) | (pl.use_k1 ? 1 << PATTN_KERNEL_PREFILL : 0) |
          (pl.use_k2 ? (1 << PATTN_KERNEL_DECODE) | (pl.fuse_reduce ? 0 : 1 << PATTN_KERNEL_REDUCE) : 0) |
-         (pl.use_k4 ? 1 << PATTN_KERNEL_GENERIC : 0);
+         (pl.use_k4 ? 1 << PATTN_KERNEL_GENERIC : 0) | (pl.use_k7 ? 1 << PATTN_KERNEL_BASELINE : 0);
 }
 
 pattn_status_t pattn_write_kv(const pattn_problem_t* p, const void* k_new, const void* v_new,

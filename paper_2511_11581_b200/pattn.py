@@ -32,9 +32,9 @@ STATUS = {
     7: "PATTN_ERR_CUDA",
 }
 DTYPE_F32, DTYPE_BF16 = 0, 1
-FLAG_FORCE_GENERIC, FLAG_NO_SPLIT, FLAG_FORCE_SPLIT, FLAG_SERIAL = 0x1, 0x2, 0x4, 0x8
-KERNEL_METADATA, KERNEL_PREFILL, KERNEL_DECODE, KERNEL_REDUCE, KERNEL_GENERIC, KERNEL_COUNT = range(6)
-KERNEL_NAMES = ["metadata", "prefill", "decode", "reduce", "generic"]
+FLAG_FORCE_GENERIC, FLAG_NO_SPLIT, FLAG_FORCE_SPLIT, FLAG_SERIAL, FLAG_BASELINE = 0x1, 0x2, 0x4, 0x8, 0x10
+KERNEL_METADATA, KERNEL_PREFILL, KERNEL_DECODE, KERNEL_REDUCE, KERNEL_GENERIC, KERNEL_BASELINE, KERNEL_COUNT = range(7)
+KERNEL_NAMES = ["metadata", "prefill", "decode", "reduce", "generic", "baseline"]
 
 
 class PattnError(RuntimeError):

@@ -356,3 +356,22 @@ def test_fused_segment_merge_equals_separate_reduce(flags, monkeypatch):
     again = db.run(flags=flags)
     assert torch.equal(again, fused)  # deterministic whichever CTA finishes a unit last
     monkeypatch.delenv("PATTN_K3_FUSED")
+
+
+@pytest.mark.parametrize("case", [0, 4, 5, 6, 7, 8])
+def test_baseline_kernel_parity(case):
+    """The paper's baseline kernel (App. A, PATTN_FLAG_BASELINE: one warp per (token, head),
+    tile = BLOCK_SIZE) against the oracle, bf16 and fp32, NHD / HND, block sizes 16, 80, 7, 5."""
+    heads, D, bs, dt, layout, dist = CASES[case]
+    rng = np.random.default_rng(77 + case)
+    w = random_workload(rng, heads, D, bs, dt, max_seqs=5, max_len=400, decode_share=0.5)
+    batch = generate(w, seed=case, dist=dist, layout=layout)
+    db = DeviceBatch(batch)
+    p = P.make_problem(db.q, db.k, w.num_kv_heads, w.block_size, db.bt, w.num_seqs, None, layout,
+                       flags=P.FLAG_BASELINE)
+    assert P.planned_kernels(p) == (1 << P.KERNEL_METADATA) | (1 << P.KERNEL_BASELINE)
+    _check(batch, P.FLAG_BASELINE, f"baseline case {case} {w.seqs}")
+
+
+def test_baseline_kernel_config1_fp32():
+    _check(generate(CONFIGS["c1_tiny"], seed=1001), P.FLAG_BASELINE, "baseline c1")
