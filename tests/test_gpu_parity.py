@@ -293,7 +293,13 @@ def test_full_size_sampled(name):
     w = CONFIGS[name]
     batch = generate(w, seed=2000 + list(CONFIGS).index(name), dist="peaked", poison=True)
     db = DeviceBatch(batch)
-    out = out_f64(db.run()).reshape(-1, w.head_dim)
+    o_serial = db.run()
+    if any(q > 1 for _, q in w.seqs):
+        # bench's launch configuration: decode kernels on a second stream over K5's SM split;
+        # per-item arithmetic is unchanged, so the output must be bitwise the serial one
+        o_two = db.run(stream2=torch.cuda.Stream())
+        assert torch.equal(o_two, o_serial), name
+    out = out_f64(o_serial).reshape(-1, w.head_dim)
     rows = _sample_rows(batch, 2000, np.random.default_rng(3))
     ref = O.batch_attention(batch, rows=rows)
     assert_close(out[rows], ref, w.dtype, name)
