@@ -7,18 +7,25 @@
 // iterative tiled softmax":
 //     M = max_s m_s ;  w_s = 2^{m_s - M} (0 for an empty segment, m_s = -inf)
 //     out[h][:] = sum_s w_s acc_s[:] / sum_s w_s l_s
-// Segments are combined in index order (deterministic; no atomics).
-// Grid: (num_seqs, Hkv * HG, D / 32); each 64-thread CTA handles 32 head-dim lanes of the
-// <= 8 query heads of one (sequence, KV head, head group); non-decode or unsplit sequences
-// exit at once.
+// Segments are combined in a fixed order (deterministic; no atomics).
+// Grid: (num_seqs, Hkv * HG, D / 32); each CTA handles 32 head-dim lanes of the <= 8 query
+// heads of one (sequence, KV head, head group); non-decode or unsplit sequences exit at once.
 #include "common.cuh"
 #include "kernels.h"
 
 namespace pattn {
 namespace {
 
-template <int D>
-__global__ void __launch_bounds__(64) k3_reduce(Params p) {
+// SG x 64 threads = SG segment groups x 8 heads x 8 float4 columns: thread (sg, h, d4) reduces
+// the segments s = sg (mod SG) of head h for columns 4*d4 .. 4*d4+3 of the CTA's 32-column
+// slice, then the groups are combined through shared memory in group order (deterministic).
+// SG = 4 for long contexts (config 4: 37 segments per unit; the reduce went 17 -> 11 us), SG = 1
+// when segments are few (config 2: 5 segments; four groups only added threads and barriers).
+template <int D, int kSegGroups>
+__global__ void __launch_bounds__(64 * kSegGroups) k3_reduce(Params p) {
+  __shared__ float s_max[kSegGroups][8];
+  __shared__ float4 s_num[kSegGroups][8][8];
+  __shared__ float s_den[kSegGroups][8];
   const int b = blockIdx.x;
   const int qb = p.cu_seqlens_q[b + 1] - p.cu_seqlens_q[b];
   if (!(p.decode_to_k2 && qb == 1)) return;
@@ -29,30 +36,55 @@ __global__ void __launch_bounds__(64) k3_reduce(Params p) {
   const int g_eff = min(8, p.G - hg * 8);
   const int head0 = kvh * p.G + hg * 8;
   const int tok = p.cu_seqlens_q[b];
-  __nv_bfloat16* O = static_cast<__nv_bfloat16*>(p.out);
-  for (int idx = threadIdx.x; idx < g_eff * 8; idx += blockDim.x) {
-    const int h = head0 + idx / 8;
-    const int d4 = blockIdx.z * 8 + idx % 8;
-    float M = -INFINITY;
-    for (int c = 0; c < n; ++c) M = fmaxf(M, p.part_m[(int64_t)(c0 + c) * p.Hq + h]);
-    float den = 0.f;
-    float4 num = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int c = 0; c < n; ++c) {
-      const int64_t row = (int64_t)(c0 + c) * p.Hq + h;
+  const int d4 = threadIdx.x & 7, h = (threadIdx.x >> 3) & 7, sg = threadIdx.x >> 6;
+  const bool active = h < g_eff;
+  const int d4g = blockIdx.z * 8 + d4;  // float4 column within the head
+  // 1. M = max_s m_s per head (each group over its segments, then across groups)
+  float M = -INFINITY;
+  if (active)
+    for (int c = sg; c < n; c += kSegGroups) M = fmaxf(M, p.part_m[(int64_t)(c0 + c) * p.Hq + head0 + h]);
+  if (d4 == 0) s_max[sg][h] = M;
+  __syncthreads();
+#pragma unroll
+  for (int g = 0; g < kSegGroups; ++g) M = fmaxf(M, s_max[g][h]);
+  // 2. w_s = 2^{m_s - M} (0 for an empty segment); num = sum w_s acc_s, den = sum w_s l_s
+  float den = 0.f;
+  float4 num = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (active) {
+#pragma unroll 4
+    for (int c = sg; c < n; c += kSegGroups) {
+      const int64_t row = (int64_t)(c0 + c) * p.Hq + head0 + h;
       const float mc = p.part_m[row];
       const float w = (mc == -INFINITY) ? 0.f : exp2f(mc - M);
       den = fmaf(w, p.part_l[row], den);
-      const float4 a = reinterpret_cast<const float4*>(p.part_acc + row * D)[d4];
+      const float4 a = reinterpret_cast<const float4*>(p.part_acc + row * D)[d4g];
       num.x = fmaf(w, a.x, num.x);
       num.y = fmaf(w, a.y, num.y);
       num.z = fmaf(w, a.z, num.z);
       num.w = fmaf(w, a.w, num.w);
     }
-    const float inv = 1.f / den;
+  }
+  s_num[sg][h][d4] = num;
+  if (d4 == 0) s_den[sg][h] = den;
+  __syncthreads();
+  if (sg == 0 && active) {
+    float4 t = s_num[0][h][d4];
+    float dd = s_den[0][h];
+#pragma unroll
+    for (int g = 1; g < kSegGroups; ++g) {
+      const float4 u = s_num[g][h][d4];
+      t.x += u.x;
+      t.y += u.y;
+      t.z += u.z;
+      t.w += u.w;
+      dd += s_den[g][h];
+    }
+    const float inv = 1.f / dd;
     uint2 packed;
-    packed.x = pack_bf16(num.x * inv, num.y * inv);
-    packed.y = pack_bf16(num.z * inv, num.w * inv);
-    *reinterpret_cast<uint2*>(O + (int64_t)tok * p.o_st_tok + (int64_t)h * p.o_st_head + d4 * 4) = packed;
+    packed.x = pack_bf16(t.x * inv, t.y * inv);
+    packed.y = pack_bf16(t.z * inv, t.w * inv);
+    __nv_bfloat16* O = static_cast<__nv_bfloat16*>(p.out);
+    *reinterpret_cast<uint2*>(O + (int64_t)tok * p.o_st_tok + (int64_t)(head0 + h) * p.o_st_head + d4g * 4) = packed;
   }
 }
 
@@ -60,12 +92,20 @@ __global__ void __launch_bounds__(64) k3_reduce(Params p) {
 
 cudaError_t launch_reduce(const Params& p, cudaStream_t stream) {
   dim3 grid(p.B, p.Hkv * p.HG, p.D / 32);
-  if (p.D == 64)
-    k3_reduce<64><<<grid, 64, 0, stream>>>(p);
-  else if (p.D == 128)
-    k3_reduce<128><<<grid, 64, 0, stream>>>(p);
-  else
+  const bool many = p.max_seq_len_hint > 16384;  // long contexts split into many segments
+  if (p.D == 64) {
+    if (many)
+      k3_reduce<64, 4><<<grid, 256, 0, stream>>>(p);
+    else
+      k3_reduce<64, 1><<<grid, 64, 0, stream>>>(p);
+  } else if (p.D == 128) {
+    if (many)
+      k3_reduce<128, 4><<<grid, 256, 0, stream>>>(p);
+    else
+      k3_reduce<128, 1><<<grid, 64, 0, stream>>>(p);
+  } else {
     return cudaErrorInvalidValue;
+  }
   return cudaGetLastError();
 }
 

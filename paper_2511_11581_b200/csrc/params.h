@@ -64,7 +64,8 @@ struct Params {
   float* part_l;      // [max_chunks][Hq]
   float* part_acc;    // [max_chunks][Hq][D]
   int32_t* seg_cnt;   // [B][Hkv*HG] segments finished per decode unit (fused merge; zeroed by K5)
-  int32_t fuse_reduce;  // 1: the CTA finishing a unit's last segment merges the partials (no K3)
+  int32_t fuse_reduce;
+  int32_t max_seq_len_hint;  // host hint (max_seq_len, else max_blocks_per_seq * block_size)  // 1: the CTA finishing a unit's last segment merges the partials (no K3)
 };
 
 }  // namespace pattn

@@ -189,6 +189,7 @@ void fill_params(const pattn_problem_t* p, const Plan& pl, Params* k) {
   k->kv_st_tok = p->kv_stride_tok;
   k->kv_st_head = p->kv_stride_head;
   k->bt_stride = p->bt_stride;
+  k->max_seq_len_hint = p->max_seq_len > 0 ? p->max_seq_len : p->max_blocks_per_seq * p->block_size;
   k->o_st_tok = p->o_stride_tok;
   k->o_st_head = p->o_stride_head;
 }
