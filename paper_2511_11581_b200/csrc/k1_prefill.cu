@@ -104,6 +104,11 @@ constexpr int kVStages = PATTN_K1_VST;  // V waits on PV (later than S), so it g
 #define PATTN_K1_PINGPONG 0  // measured slower: off
 #endif
 constexpr int kBarExpA = 1, kBarExpB = 2;
+// Load the next tile's S from TMEM as soon as the current tile's exponentials are done, when
+// it is already complete (non-blocking test), instead of after this tile's P store.
+#ifndef PATTN_K1_SPREFETCH
+#define PATTN_K1_SPREFETCH 0  // measured: 791 vs 939 TFLOP/s (register spills), off
+#endif
 // P -> bf16 with integer ops (round half up on the fp32 bits, then a byte permute) instead of
 // F2FP: F2FP issues on the same XU pipe as MUFU.EX2 (measured 8 clk per warp instruction per
 // SMSP for both, scripts/micro/pipes.cu), i.e. one third of the softmax's XU time.
@@ -565,12 +570,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int row_lim = min(x.ctx + x.tok0 + tk + 1, x.kv_end);  // keys [0, row_lim) visible
       const int nsb_valid = (x.kv_end + 15) / 16;                  // 16-key sub-blocks fetched
       float m_run = -INFINITY, l_run = 0.f;
+      float s[kN];
+      bool s_loaded = false;  // S of this tile already requested by the previous iteration
       for (int jt = 0; jt < x.ntiles; ++jt) {
         const int sb = jt & 1;  // S buffer of this tile (P is written back over it)
         const uint32_t tS = tS0 + 64 * sb;
-        mbar_wait(&bar.s_full[h][sb], (sb ? sc1 : sc0) & 1u);
-        sc0 += sb ? 0u : 1u;
-        sc1 += sb ? 1u : 0u;
+        if (!s_loaded) {
+          mbar_wait(&bar.s_full[h][sb], (sb ? sc1 : sc0) & 1u);
+          sc0 += sb ? 0u : 1u;
+          sc1 += sb ? 1u : 0u;
+        }
         if (r == 0) PATTN_K1_TRACE(10 + h);
         tc_fence_after();
 #ifdef PATTN_K1_NOSOFTMAX  // timing experiment only: P = bf16 pairs of S, no max / exp / rescale
@@ -589,13 +598,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           continue;
         }
 #endif
-        float s[kN];
         {
           uint32_t* su = reinterpret_cast<uint32_t*>(s);
-          PATTN_TMEM_LD32(tS + 0, (su + 0));
-          PATTN_TMEM_LD32(tS + 32, (su + 32));
+          if (!s_loaded) {
+            PATTN_TMEM_LD32(tS + 0, (su + 0));
+            PATTN_TMEM_LD32(tS + 32, (su + 32));
+          }
           tmem_wait_ld();
         }
+        s_loaded = false;
         if (r == 0) PATTN_K1_TRACE(30 + h);
         const int key0 = jt * kN;
         const int nvis = row_lim - key0;  // keys [key0, key0 + nvis) of this tile are visible
@@ -653,6 +664,24 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
         }
         if (PATTN_K1_PINGPONG) named_bar_arrive(h ? kBarExpA : kBarExpB, 2 * kHalfM);
+#if PATTN_K1_SPREFETCH
+        // s[] is dead now: if the next tile's S is already complete, request it from TMEM so
+        // that its load latency hides behind this tile's PV wait, rescale and P store (the
+        // test is made warp-uniform: tcgen05.ld is warp-collective)
+        if (jt + 1 < x.ntiles) {
+          const int nb = (jt + 1) & 1;
+          const bool ready = __all_sync(0xffffffffu, mbar_test(&bar.s_full[h][nb], (nb ? sc1 : sc0) & 1u));
+          if (ready) {
+            sc0 += nb ? 0u : 1u;
+            sc1 += nb ? 1u : 0u;
+            tc_fence_after();
+            uint32_t* su = reinterpret_cast<uint32_t*>(s);
+            PATTN_TMEM_LD32(tS0 + 64 * nb + 0, (su + 0));
+            PATTN_TMEM_LD32(tS0 + 64 * nb + 32, (su + 32));
+            s_loaded = true;
+          }
+        }
+#endif
         const uint64_t r01 = fadd2(rs2[0], rs2[1]), r23 = fadd2(rs2[2], rs2[3]), rr = fadd2(r01, r23);
         const float rs = f32x2_lo(rr) + f32x2_hi(rr);
         if (r == 0) PATTN_K1_TRACE(34 + h);
