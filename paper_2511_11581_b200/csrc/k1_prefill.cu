@@ -80,7 +80,16 @@ constexpr int kHalfM = 128;    // rows per half (one UMMA M)
 constexpr int kM = 2 * kHalfM; // BLOCK_M
 constexpr int kN = 64;         // keys per KV tile
 constexpr int kD = 128;        // head dim
-constexpr int kThreads = 512;  // 16 warps
+// Column split (experiment): 8 more softmax warps (16-23, "part B") take key columns 32-63 of
+// every 64-key tile of their half; part A (warps 4-11) keeps columns 0-31 and all O work.
+// Row maxima are exchanged per tile through shared memory (16-bit, rounded up) between the
+// two warps of a TMEM lane quadrant; B's row sum is handed to A at the end of the item.
+#ifndef PATTN_K1_COLSPLIT
+#define PATTN_K1_COLSPLIT 0
+#endif
+constexpr bool kColSplit = PATTN_K1_COLSPLIT != 0;
+constexpr int kThreads = kColSplit ? 768 : 512;  // 24 / 16 warps
+constexpr int kNc = kColSplit ? 32 : 64;         // key columns per softmax warp
 constexpr uint32_t kQTile = kHalfM * kD * 2;  // 32 KB: one 128-row half of the Q block
 constexpr uint32_t kHalf = kQTile / 2;         // 16 KB: one 64-wide d half of it
 constexpr uint32_t kTile = kN * kD * 2;        // 16 KB: one K or V tile (64 keys)
@@ -135,8 +144,9 @@ constexpr uint32_t kStageWarp = PATTN_K1_STAGE_FULL ? 8192 : 4096;
 constexpr uint32_t kStageHalf = 4 * kStageWarp;
 constexpr uint32_t kOffStage = kOffV + kVStages * kTile;
 constexpr uint32_t kOffBar = kOffStage + 2 * kStageHalf;
-constexpr uint32_t kBarBlock = 1024;  // barriers + the item ring
-constexpr uint32_t kSmemBytes = kOffBar + kBarBlock + 1024;
+constexpr uint32_t kBarBlock = 512;  // barriers + the item ring
+constexpr uint32_t kOffX = kOffBar + kBarBlock;  // column-split exchange: 16-bit maxima / fp32 row sums
+constexpr uint32_t kSmemBytes = kOffX + (kColSplit ? 1024 : 0) + 1024;
 static_assert(kSmemBytes <= 227 * 1024, "shared memory budget");
 
 // TMEM columns
@@ -170,7 +180,7 @@ constexpr int kMmaWarps = PATTN_K1_SPLIT_MMA ? 2 : 1;
 #ifndef PATTN_K1_SKEW_CLK
 #define PATTN_K1_SKEW_CLK 0
 #endif
-constexpr int kItemConsumers = 14 + (kMmaWarps - 1);  // warps 0-3, 12, 14, (15) and the 8 softmax warps
+constexpr int kItemConsumers = 14 + (kMmaWarps - 1) + (kColSplit ? 8 : 0);  // warps 0-3, 12, 14, (15) and the 8 softmax warps
 
 struct Item {
   int b, kvh, q0, qlen, L, ctx, tok0, ntok, kv_end, ntiles;
@@ -305,7 +315,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int h = 0; h < 2; ++h) {
       mbar_init(&bar.s_full[h][0], 1);
       mbar_init(&bar.s_full[h][1], 1);
-      mbar_init(&bar.p_full[h], kHalfM);
+      mbar_init(&bar.p_full[h], kColSplit ? 2 * kHalfM : kHalfM);
       mbar_init(&bar.pv_done[h], 1);
       mbar_init(&bar.o_empty[h], kHalfM);
     }
@@ -483,7 +493,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp >= 13) {
+  } else if (warp == 13 || warp == 14) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");  // warpgroup 3 (13, 14)
     if (warp == 13) {
       // ================================================================ item scheduler
@@ -548,9 +558,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ================================================================ softmax / correction / epilogue
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 208;\n" ::: "memory");
-    const int h = (warp - 4) >> 2;             // half a (0) or b (1)
-    const int r = threadIdx.x - 128 - h * 128;  // row within the half == TMEM lane
+    if constexpr (kColSplit)
+      asm volatile("setmaxnreg.inc.sync.aligned.u32 96;\n" ::: "memory");  // 128*56 + 128*40 + 512*96 = 80*768
+    else
+      asm volatile("setmaxnreg.inc.sync.aligned.u32 208;\n" ::: "memory");
+    const int part = (kColSplit && warp >= 16) ? 1 : 0;      // key columns [32 part, +kNc)
+    const int h = part ? (warp - 16) >> 2 : (warp - 4) >> 2;  // half a (0) or b (1)
+    const int r = 32 * (warp & 3) + lane;                      // row within the half == TMEM lane
+    const int colb = part * kNc;
+    const int xbar = 3 + h * 4 + (warp & 3);  // named barrier of the (A, B) warp pair (column split)
+    uint16_t* xs = reinterpret_cast<uint16_t*>(smem + kOffX);
+    float* xf = reinterpret_cast<float*>(smem + kOffX);
     const uint32_t lane_off = (uint32_t)(32 * (warp & 3)) << 16;
     const uint32_t tS0 = tmem + kTmemS + 128 * h + lane_off;
     const uint32_t tO = tmem + kTmemO + 128 * h + lane_off;
@@ -570,7 +588,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int row_lim = min(x.ctx + x.tok0 + tk + 1, x.kv_end);  // keys [0, row_lim) visible
       const int nsb_valid = (x.kv_end + 15) / 16;                  // 16-key sub-blocks fetched
       float m_run = -INFINITY, l_run = 0.f;
-      float s[kN];
+      float s[kNc];
       bool s_loaded = false;  // S of this tile already requested by the previous iteration
       for (int jt = 0; jt < x.ntiles; ++jt) {
         const int sb = jt & 1;  // S buffer of this tile (P is written back over it)
@@ -601,8 +619,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         {
           uint32_t* su = reinterpret_cast<uint32_t*>(s);
           if (!s_loaded) {
-            PATTN_TMEM_LD32(tS + 0, (su + 0));
-            PATTN_TMEM_LD32(tS + 32, (su + 32));
+            PATTN_TMEM_LD32(tS + colb, (su + 0));
+            if constexpr (kNc == 64) PATTN_TMEM_LD32(tS + 32, (su + 32));
           }
           tmem_wait_ld();
         }
@@ -612,19 +630,31 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int nvis = row_lim - key0;  // keys [key0, key0 + nvis) of this tile are visible
         if (cs < 0.f) {  // sign-adjust so that max(raw) * |c| = max(scaled)
 #pragma unroll
-          for (int c = 0; c < kN; ++c) s[c] = -s[c];
+          for (int c = 0; c < kNc; ++c) s[c] = -s[c];
         }
-        if (__any_sync(0xffffffffu, nvis < kN)) {  // diagonal / tail tile: causal mask (warp-uniform)
+        if (__any_sync(0xffffffffu, nvis < colb + kNc)) {  // diagonal / tail tile: causal mask (warp-uniform)
 #pragma unroll
-          for (int c = 0; c < kN; ++c) s[c] = c < nvis ? s[c] : -INFINITY;
+          for (int c = 0; c < kNc; ++c) s[c] = c + colb < nvis ? s[c] : -INFINITY;
         }
         float mx[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) mx[i] = s[i];
 #pragma unroll
-        for (int c = 8; c < kN; ++c) mx[c & 7] = fmaxf(mx[c & 7], s[c]);
-        const float mraw = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
-                                 fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+        for (int c = 8; c < kNc; ++c) mx[c & 7] = fmaxf(mx[c & 7], s[c]);
+        float mraw = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                           fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+        if constexpr (kColSplit) {
+          // both warps of the pair must use the same row max: exchange 16-bit values rounded
+          // toward +inf (any upper bound of the row max is a valid shift) and take the max
+          uint32_t u = __float_as_uint(mraw);
+          u = (int32_t)u >= 0 && (u & 0xffffu) ? u + 0x10000u : u;
+          const uint16_t mine = (uint16_t)(u >> 16);
+          named_bar_sync(xbar, 64);  // the partner has read the previous value
+          xs[(h * 2 + part) * kHalfM + r] = mine;
+          named_bar_sync(xbar, 64);
+          const uint16_t other = xs[(h * 2 + (part ^ 1)) * kHalfM + r];
+          mraw = fmaxf(__uint_as_float((uint32_t)mine << 16), __uint_as_float((uint32_t)other << 16));
+        }
         if (r == 0) PATTN_K1_TRACE(32 + h);
         const float mt = mraw * ca;
         const float m_new = fmaxf(m_run, mt);
@@ -638,11 +668,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         // exponent argument and the row sum
         const uint64_t ca2 = f32x2(ca, ca), nb2 = f32x2(nbase, nbase);
         uint64_t rs2[4] = {0ull, 0ull, 0ull, 0ull};
-        uint32_t pk[kN / 2];
+        uint32_t pk[kNc / 2];
         // both halves see the same number of tiles per item, so the turns strictly alternate
         if (PATTN_K1_PINGPONG) named_bar_sync(h ? kBarExpB : kBarExpA, 2 * kHalfM);
 #pragma unroll
-        for (int c = 0; c < kN; c += 2) {
+        for (int c = 0; c < kNc; c += 2) {
           // e^{scale*qk - m} in the log2 domain
           const uint64_t xx = ffma2(f32x2(s[c], s[c + 1]), ca2, nb2);
           uint64_t ee;
@@ -687,7 +717,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (r == 0) PATTN_K1_TRACE(34 + h);
         // O_h: PV_h(jt-1) (issued once P_h(jt-1) arrived, while this tile's exponentials ran)
         // must be complete before O_h is corrected and before P_h(jt) can be consumed.
-        if (jt > 0) {
+        if (part == 0 && jt > 0) {
           mbar_wait(&bar.pv_done[h], (tc - 1) & 1u);
           tc_fence_after();
           // tcgen05.ld/st are warp-collective (.sync.aligned): rescale when ANY row of the warp needs it
@@ -706,11 +736,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         l_run = l_run * alpha + rs;
         m_run = m_use;
         // P (bf16, 2 per column) over the first 32 columns of the S buffer: the A operand of PV_h
-        PATTN_TMEM_ST32(tS + 0, (pk + 0));
+        if constexpr (kColSplit)
+          PATTN_TMEM_ST16(tS + part * 16, (pk + 0));
+        else
+          PATTN_TMEM_ST32(tS + 0, (pk + 0));
         // Zero V rows of slots >= L inside the last fetched sub-block (they may hold NaN).  With
         // one MMA warp, WG a does it (PV_b is issued after PV_a); with one MMA warp per half
         // each WG does it before releasing its own P (both write the same zeros).
-        if (h == 0 || PATTN_K1_SPLIT_MMA) {
+        if ((h == 0 || PATTN_K1_SPLIT_MMA) && part == 0) {
           const int z0 = x.L - key0, z1 = min(kN, nsb_valid * 16 - key0);
           if (z0 < z1 && z0 < kN) {
             const uint32_t s2 = vc % kVStages;
@@ -730,6 +763,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (r == 0) PATTN_K1_TRACE(12 + h);
         mbar_arrive(&bar.p_full[h]);
         ++tc;
+      }
+      if constexpr (kColSplit) {  // B hands its partial row sum to A, which does the epilogue
+        named_bar_sync(xbar, 64);   // A has read B's last row max
+        if (part == 1) xf[h * kHalfM + r] = l_run;
+        named_bar_sync(xbar, 64);
+        if (part == 1) continue;
+        l_run += xf[h * kHalfM + r];
       }
       // ---- epilogue: O / l -> bf16 -> out (valid rows only)
       mbar_wait(&bar.pv_done[h], (tc - 1) & 1u);
