@@ -66,7 +66,7 @@ def main(rnd):
                 name = {"k1_prefill": "prefill", "k2_decode": "decode", "k3_reduce": "reduce",
                         "k4_generic": "generic", "k5_metadata": "metadata"}.get(k, k)
                 traffic.setdefault(wl, {})[name] = (sum(rd) + sum(wr)) / n
-    for rep in ("k1_c3_full", "k2_c2_full"):
+    for rep in ("k1_c3_full", "k2_c2_full", "k2_c4_full", "k3_c4_full", "k6_c3_full"):
         path = os.path.join(src, rep + ".ncu-rep")
         if os.path.exists(path):
             shutil.copy(path, os.path.join(dst, rep + ".ncu-rep"))
