@@ -43,7 +43,7 @@ namespace {
 constexpr int kSub = 16;  // keys per ring stage (one mma M tile)
 constexpr int kItemRing = 16;
 #ifndef PATTN_K2_NP
-#define PATTN_K2_NP 2
+#define PATTN_K2_NP 4  // measured: per-SM decode rate +8% on 36 SMs vs 2 producers
 #endif
 constexpr int kNP = PATTN_K2_NP;  // producer warps
 constexpr size_t kItemRingBytes = kItemRing * (2 * sizeof(uint64_t) + sizeof(int));
