@@ -90,6 +90,19 @@ constexpr int kD = 128;        // head dim
 constexpr bool kColSplit = PATTN_K1_COLSPLIT != 0;
 constexpr int kThreads = kColSplit ? 768 : 512;  // 24 / 16 warps
 constexpr int kNc = kColSplit ? 32 : 64;         // key columns per softmax warp
+// setmaxnreg budgets (16-warp layout): warpgroup 0 (producers, MMA a), warpgroups 1-2
+// (softmax), warpgroup 3 (V producer, scheduler, Q producer, MMA b); 128 (a + d) + 256 s = 65536
+#ifndef PATTN_K1_REG_WG0
+#define PATTN_K1_REG_WG0 56
+#endif
+#ifndef PATTN_K1_REG_SOFTMAX
+#define PATTN_K1_REG_SOFTMAX 208
+#endif
+#ifndef PATTN_K1_REG_WG3
+#define PATTN_K1_REG_WG3 40
+#endif
+constexpr int kRegWG0 = PATTN_K1_REG_WG0, kRegSoftmax = PATTN_K1_REG_SOFTMAX, kRegWG3 = PATTN_K1_REG_WG3;
+static_assert(kColSplit || 128 * (kRegWG0 + kRegWG3) + 256 * kRegSoftmax <= 65536, "register budget");
 constexpr uint32_t kQTile = kHalfM * kD * 2;  // 32 KB: one 128-row half of the Q block
 constexpr uint32_t kHalf = kQTile / 2;         // 16 KB: one 64-wide d half of it
 constexpr uint32_t kTile = kN * kD * 2;        // 16 KB: one K or V tile (64 keys)
@@ -346,9 +359,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     // still in use by PV never delays the next K tile the S MMA waits for) and the per-box
     // TMA issue cost (~150 clk) is spread over four warps.
     if (warp < 4)
-      asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kRegWG0) : "memory");
     else
-      asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kRegWG3) : "memory");
     const int kv = (warp == 3 || warp == 12) ? 1 : 0;
     const bool owner = warp == 0 || warp == 3;  // arms the stage barrier with the tile's byte count
     const int i_lo = owner ? 0 : kN / 32, i_hi = i_lo + kN / 32;  // 2 sub-blocks per warp
@@ -403,9 +416,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     // warps, warp 1 issues half a's S and PV and warp 15 half b's; K / V / Q stages are
     // released when both have committed (the empty barriers count kMmaWarps arrivals).
     if (warp == 1)
-      asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kRegWG0) : "memory");
     else
-      asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");  // warpgroup 3
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kRegWG3) : "memory");  // warpgroup 3
     const int h_lo = (PATTN_K1_SPLIT_MMA && warp == 15) ? 1 : 0;
     const int h_hi = PATTN_K1_SPLIT_MMA ? h_lo + 1 : 2;
     constexpr uint32_t idS = idesc_bf16_f32(kHalfM, kN, 0, 0);   // Q (K-major) x K (K-major)
@@ -494,7 +507,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 13 || warp == 14) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");  // warpgroup 3 (13, 14)
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kRegWG3) : "memory");  // warpgroup 3 (13, 14)
     if (warp == 13) {
       // ================================================================ item scheduler
       const int n16 = p.bs / 16;
@@ -561,7 +574,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if constexpr (kColSplit)
       asm volatile("setmaxnreg.inc.sync.aligned.u32 96;\n" ::: "memory");  // 128*56 + 128*40 + 512*96 = 80*768
     else
-      asm volatile("setmaxnreg.inc.sync.aligned.u32 208;\n" ::: "memory");
+      asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kRegSoftmax) : "memory");
     const int part = (kColSplit && warp >= 16) ? 1 : 0;      // key columns [32 part, +kNc)
     const int h = part ? (warp - 16) >> 2 : (warp - 4) >> 2;  // half a (0) or b (1)
     const int r = 32 * (warp & 3) + lane;                      // row within the half == TMEM lane
