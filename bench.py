@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-sub", action="store_true", help="skip the keyed sub-results (other configs)")
     ap.add_argument("--streams", type=int, default=2,
                     help="2 (default): decode kernels on a second stream, concurrent with prefill; 1: serial")
     ap.add_argument("--flags", type=int, default=0)
@@ -178,11 +179,13 @@ def host_inputs_from_device(inp):
     )
 
 
-def cpu_baseline(w, inp, target_s=12.0):
+def cpu_baseline(w, seed, dev, target_s=12.0):
+    """The fp64 oracle on this host's cores, on the same inputs (regenerated from the seed)."""
     from oracle import attention as O
+    from workloads.gen import generate_device
 
     cores = len(os.sched_getaffinity(0))
-    host = host_inputs_from_device(inp)
+    host = host_inputs_from_device(generate_device(w, seed=seed, device=dev))
     rng = np.random.default_rng(7)
     oracle_sample(w, host, 8, rng, cores)  # first touch of the widened host arrays
     t_cal, n_cal = oracle_sample(w, host, 32, rng, cores)
@@ -248,6 +251,208 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------------------- our arm
+class Case:
+    """One workload resident on the device (inputs > L2, or rotated replicas of it) plus the
+    unified call over it.  `step(i)` enqueues call i (replica i mod R)."""
+
+    def __init__(self, w, seed, dev, pattn, streams, flags, l2_bytes, inp=None):
+        import torch
+
+        from workloads.gen import generate_device
+
+        self.w, self.dev, self.pattn, self.flags = w, dev, pattn, flags
+        first = inp if inp is not None else generate_device(w, seed=seed, device=dev)
+        ws_bytes = sum(first[k].numel() * first[k].element_size() for k in ("q", "k_cache", "v_cache"))
+        # working set below 2 x L2: rotate R input replicas so every call misses L2
+        self.replicas = 1 if ws_bytes >= 2 * l2_bytes else int(math.ceil(2 * l2_bytes / max(ws_bytes, 1)))
+        self.inps = [first] + [generate_device(w, seed=seed + 7919 * r, device=dev) for r in range(1, self.replicas)]
+        self.ws_bytes = ws_bytes
+        self.outs = [torch.empty_like(i["q"]) for i in self.inps]
+        self.max_q = max(qq for _, qq in w.seqs)
+        self.max_L = max(c + qq for c, qq in w.seqs)
+        i0 = self.inps[0]
+        self.prob = pattn.make_problem(i0["q"], i0["k_cache"], w.num_kv_heads, w.block_size, i0["block_table"],
+                                       w.num_seqs, self.outs[0], "NHD", self.max_q, self.max_L, flags)
+        self.stream = torch.cuda.current_stream(dev)
+        self.stream2 = torch.cuda.Stream(dev) if streams == 2 else None
+        self.streams = streams
+        nbytes = pattn.workspace_size(self.prob)
+        self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+
+    @property
+    def out(self):
+        return self.outs[0]
+
+    def step(self, i=0, events=None, stream=None, stream2=None):
+        r = i % self.replicas
+        x, w = self.inps[r], self.w
+        self.pattn.unified_attention(
+            x["q"], x["k_cache"], x["v_cache"], x["block_table"], x["cu_seqlens_q"], x["seq_lens"], w.scale,
+            w.num_kv_heads, w.block_size, self.outs[r], max_query_len=self.max_q, max_seq_len=self.max_L,
+            flags=self.flags, workspace=self.workspace, stream=stream or self.stream,
+            stream2=stream2 if stream is not None else self.stream2, events=events)
+
+    def prefill_sms(self):
+        return self.pattn.workspace_prefill_sms(self.workspace)
+
+
+def timed(case, K, W, barrier, with_events=True):
+    """W untimed calls, then K calls between CUDA events on the launching stream (barrier +
+    synchronize on both sides); per-kernel averages from the library's event hooks."""
+    import torch
+
+    pattn = case.pattn
+    for i in range(max(3, W)):
+        case.step(i)
+    torch.cuda.synchronize()
+    kev = pattn.make_events(K) if with_events else None
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    t0.record(case.stream)
+    for i in range(K):
+        case.step(i, events=kev[i] if kev else None)
+    t1.record(case.stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms = t0.elapsed_time(t1) / K
+    kern_ms = {}
+    if kev:
+        kmask = pattn.planned_kernels(case.prob)
+        for k in range(pattn.KERNEL_COUNT):
+            if kmask & (1 << k):
+                kern_ms[pattn.KERNEL_NAMES[k]] = sum(kev[i][2 * k].elapsed_time(kev[i][2 * k + 1])
+                                                     for i in range(K)) / K
+    return ms, kern_ms
+
+
+def roofline_of(case, ms, kern_ms, peaks, num_sms, traffic):
+    """Per-kernel roofline entries: algorithmic work / the kernel's average event time / the
+    FULL measured peak of the GPU (MEASURED_PEAKS.json).  With two streams K1 runs on the P SMs
+    K5 gave it; the fraction of that share's roof is reported separately (`frac_of_sm_share`)."""
+    work = kernel_work(case.w)
+    rl = {}
+    pre_name = "prefill" if "prefill" in kern_ms else ("generic" if "generic" in kern_ms else None)
+    if pre_name and work["prefill_flops"] > 0:
+        t = kern_ms[pre_name] * 1e-3
+        a = work["prefill_flops"] / t / 1e12
+        pk = peaks["bf16"]
+        e = {"bound": "tensor", "achieved": a, "peak": pk, "unit": "TFLOP/s", "frac": a / pk,
+             "traffic": traffic.get(pre_name), "kernel": pre_name, "kernel_ms": kern_ms[pre_name],
+             "share_of_step": kern_ms[pre_name] / ms,
+             "algorithmic_unit": "4*D*Hq*(ctx_b+i+1) flop per prefill query token (visible pairs only)"}
+        if pre_name == "prefill" and case.streams == 2 and "decode" in kern_ms:
+            sms = case.prefill_sms()
+            e["prefill_sms"] = sms
+            e["frac_of_sm_share"] = a / (pk * sms / num_sms)
+        rl["prefill"] = e
+    if "decode" in kern_ms and work["decode_bytes"] > 0:
+        t = kern_ms["decode"] * 1e-3
+        a = work["decode_bytes"] / t / 1e9
+        rl["decode"] = {"bound": "hbm", "achieved": a, "peak": peaks["hbm"], "unit": "GB/s", "frac": a / peaks["hbm"],
+                        "traffic": traffic.get("decode"), "kernel": "decode", "kernel_ms": kern_ms["decode"],
+                        "share_of_step": kern_ms["decode"] / ms,
+                        "algorithmic_unit": "L_b*Hkv*2*D*2 B of K+V + 2*Hq*D*2 B of q/out per decode sequence"}
+    if "baseline" in kern_ms:  # the paper's App. A kernel (--flags 16): SIMT, reported by time only
+        rl["baseline"] = {"bound": "alu", "achieved": work["total_flops"] / (kern_ms["baseline"] * 1e-3) / 1e12,
+                          "peak": None, "unit": "TFLOP/s", "frac": None, "traffic": None, "kernel": "baseline",
+                          "kernel_ms": kern_ms["baseline"], "share_of_step": kern_ms["baseline"] / ms}
+    return rl
+
+
+def sub_result(name, w, dev, pattn, streams, K, W, peaks, num_sms, l2, barrier, seed):
+    """A second workload timed in the same run (keyed sub-result of the JSON line)."""
+    import torch
+
+    case = Case(w, seed, dev, pattn, streams, 0, l2)
+    ms, kern_ms = timed(case, K, W, barrier)
+    rl = roofline_of(case, ms, kern_ms, peaks, num_sms, load_traffic(name))
+    dom = max(rl.values(), key=lambda r: r["kernel_ms"]) if rl else None
+    r = {"workload": name, "streams": streams, "ms_per_step": ms, "value": w.num_tokens / (ms * 1e-3),
+         "unit": "tokens/s", "kernel_ms": kern_ms, "replicas": case.replicas,
+         "l2": "inputs %.2f GB %s" % (case.ws_bytes / 1e9, "> 2x L2, no flush" if case.replicas == 1 else
+                                      f"< 2x L2: {case.replicas} rotated replicas"),
+         "roofline": ({k: dom[k] for k in ("bound", "achieved", "peak", "unit", "frac", "traffic", "kernel")}
+                      if dom else None)}
+    del case
+    torch.cuda.empty_cache()
+    return r
+
+
+def strong_scaling_c5(args, dev, pattn, world, rank, barrier, l2):
+    """Config 5 (256 sequences, 70B heads) as ONE global batch split over the ranks by sequence
+    and by KV head (shard.py; no collective on the timed path).  Each rank generates the same
+    global batch (same seed), builds its shard, and the shards are timed together (max over
+    ranks).  Verification (untimed): the shards' outputs are all-gathered over NCCL and rank 0
+    compares them with its own unsharded single-GPU output of the global batch."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2511_11581_b200 import shard
+    from workloads import CONFIGS
+    from workloads.gen import generate_device
+
+    w = CONFIGS["c5_mixed70b"]
+    K = min(args.steps, 50)
+    g = generate_device(w, seed=args.seed + 555, device=dev)
+    res = {"workload": "c5_mixed70b", "global_tokens": w.num_tokens}
+    # P = 1 point of the curve: the whole batch on this GPU (rank 0; the others wait)
+    ref = None
+    if rank == 0:
+        full = Case(w, 0, dev, pattn, 2, 0, l2, inp=g)
+        ms1, _ = timed(full, K, args.warmup, lambda: None, with_events=False)
+        ref = full.out.clone()
+        res["one_gpu_ms"] = ms1
+        del full
+    barrier()
+    if world == 1:
+        res["value_one_gpu"] = w.num_tokens / (res["one_gpu_ms"] * 1e-3)
+        return res
+    cu_h, sl_h, bt_h = g["cu_seqlens_q_h"].numpy(), g["seq_lens_h"].numpy(), g["block_table_h"].numpy()
+    for mode in ("seq", "kvhead"):
+        plan = shard.plan_shards(cu_h, sl_h, w.num_q_heads, w.num_kv_heads, w.head_dim, world, mode)
+        lb = shard.local_batch(plan, rank, g["q"], g["k_cache"], g["v_cache"], bt_h, cu_h, sl_h, w.block_size, dev)
+        if mode == "kvhead":
+            lw = w.__class__(f"c5/kvhead{rank}of{world}", w.seqs, len(lb.q_heads), lb.num_kv_heads, w.head_dim,
+                             w.block_size, w.dtype)
+        else:
+            lw = w.with_seqs([w.seqs[b] for b in plan.seq_ids[rank]], name=f"c5/seq{rank}of{world}")
+        linp = dict(q=lb.q, k_cache=lb.k_cache, v_cache=lb.v_cache, block_table=lb.block_table,
+                    cu_seqlens_q=lb.cu_seqlens_q, seq_lens=lb.seq_lens)
+        case = Case(lw, 0, dev, pattn, 2, 0, l2, inp=linp)
+        ms, _ = timed(case, K, args.warmup, barrier, with_events=False)
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_max = float(t.item())
+        gathered = shard.gather_outputs(plan, case.out, cu_h, w.num_q_heads)
+        entry = {"ms_per_step": ms_max, "value": w.num_tokens / (ms_max * 1e-3), "unit": "tokens/s",
+                 "local_seqs": int(lw.num_seqs), "local_heads": f"{lw.num_q_heads}q/{lw.num_kv_heads}kv",
+                 "replicas": case.replicas}
+        if rank == 0:
+            rng = np.random.default_rng(5)
+            rows = torch.from_numpy(np.sort(rng.choice(w.num_tokens, size=min(4096, w.num_tokens), replace=False)))
+            rows = rows.to(dev)
+            a, b = gathered.index_select(0, rows).float(), ref.index_select(0, rows).float()
+            diff = (a - b).abs()
+            entry["verify"] = {
+                "rows_sampled": int(rows.numel()),
+                "bitwise_equal": bool(torch.equal(gathered.index_select(0, rows), ref.index_select(0, rows))),
+                "max_abs_diff_vs_unsharded": float(diff.max().item()),
+                # plans differ per shard (K5 sizes decode segments from the local batch), so the
+                # outputs agree to the bf16 tolerance rather than bitwise in general
+                "within_bf16_tol": bool((diff <= 1e-2 + 1e-2 * b.abs()).all().item()),
+            }
+            entry["efficiency_vs_one_gpu"] = res["one_gpu_ms"] / (world * ms_max)
+        res[mode] = entry
+        del case, lb, linp, gathered
+        torch.cuda.empty_cache()
+        barrier()
+    if rank == 0:
+        res["verified"] = all(res[m]["verify"]["within_bf16_tol"] for m in ("seq", "kvhead"))
+    return res
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -258,7 +463,7 @@ def main():
 
     from paper_2511_11581_b200 import pattn
     from workloads import CONFIGS
-    from workloads.gen import ATTRIBUTION, generate_device
+    from workloads.gen import ATTRIBUTION
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -276,59 +481,28 @@ def main():
         else:
             dist.init_process_group(backend)
     pattn.load()
-
-    w_global = CONFIGS[args.workload] if args.workload in CONFIGS else ATTRIBUTION[args.workload]
-    shard_world = args.sim_world if args.sim_world else world
-    shard_rank = args.sim_rank if args.sim_world else rank
-    w = local_workload(w_global, args.shard, shard_world, shard_rank)
-    inp = generate_device(w, seed=args.seed + rank, device=dev)
-    q, kc, vc = inp["q"], inp["k_cache"], inp["v_cache"]
-    bt, cu, sl = inp["block_table"], inp["cu_seqlens_q"], inp["seq_lens"]
-    out = torch.empty_like(q)
-    max_q = max(qq for _, qq in w.seqs)
-    max_L = max(c + qq for c, qq in w.seqs)
-    prob = pattn.make_problem(q, kc, w.num_kv_heads, w.block_size, bt, w.num_seqs, out, "NHD", max_q, max_L,
-                              args.flags)
-    launches_per_step = pattn.planned_launches(prob)
-    stream = torch.cuda.current_stream(dev)
-    stream2 = torch.cuda.Stream(dev) if args.streams == 2 else None
-
-    def step(events=None):
-        pattn.unified_attention(q, kc, vc, bt, cu, sl, w.scale, w.num_kv_heads, w.block_size, out,
-                                max_query_len=max_q, max_seq_len=max_L, flags=args.flags, stream=stream,
-                                stream2=stream2, events=events)
+    props = torch.cuda.get_device_properties(dev)
+    num_sms = props.multi_processor_count
+    l2 = int(getattr(props, "L2_cache_size", 126 << 20) or (126 << 20))
+    peaks = load_peaks()
 
     def barrier():
         if world > 1:
             dist.barrier()
 
-    for _ in range(max(3, args.warmup)):
-        step()
-    torch.cuda.synchronize()
-
+    w_global = CONFIGS[args.workload] if args.workload in CONFIGS else ATTRIBUTION[args.workload]
+    shard_world = args.sim_world if args.sim_world else world
+    shard_rank = args.sim_rank if args.sim_world else rank
+    w = local_workload(w_global, args.shard, shard_world, shard_rank)
+    case = Case(w, args.seed + rank, dev, pattn, args.streams, args.flags, l2)
+    inp = case.inps[0]
+    q, kc = inp["q"], inp["k_cache"]
+    launches_per_step = pattn.planned_launches(case.prob)
     K = args.steps
-    NK = pattn.KERNEL_COUNT
-    kmask = pattn.planned_kernels(prob)
-    kev = pattn.make_events(K)
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
     sampler = ClockSampler(local)
-    barrier()
-    torch.cuda.synchronize()
     with sampler:
-        t0.record(stream)
-        for i in range(K):
-            step(kev[i])
-        t1.record(stream)
-        torch.cuda.synchronize()
-    barrier()
-    ms = t0.elapsed_time(t1) / K
-    # K1's SM share in the timed steps (K5's two-stream partition; all SMs when serial)
-    prefill_sms_timed = pattn.last_prefill_sms(local)
-    # per-kernel average durations (only kinds that were launched)
-    kern_ms = {}
-    for k in range(NK):
-        if kmask & (1 << k):
-            kern_ms[pattn.KERNEL_NAMES[k]] = sum(kev[i][2 * k].elapsed_time(kev[i][2 * k + 1]) for i in range(K)) / K
+        ms, kern_ms = timed(case, K, args.warmup, barrier)
 
     if args.shard == "none":
         tokens_all = w.num_tokens * world  # weak scaling: every rank runs the full workload
@@ -344,15 +518,11 @@ def main():
         gs = torch.cuda.Stream(dev)
         gs2 = torch.cuda.Stream(dev) if args.streams == 2 else None
         with torch.cuda.stream(gs):
-            pattn.unified_attention(q, kc, vc, bt, cu, sl, w.scale, w.num_kv_heads, w.block_size, out,
-                                    max_query_len=max_q, max_seq_len=max_L, flags=args.flags, stream=gs,
-                                    stream2=gs2)
+            case.step(0, stream=gs, stream2=gs2)
         torch.cuda.synchronize()
         cg = torch.cuda.CUDAGraph()
         with torch.cuda.graph(cg, stream=gs):
-            pattn.unified_attention(q, kc, vc, bt, cu, sl, w.scale, w.num_kv_heads, w.block_size, out,
-                                    max_query_len=max_q, max_seq_len=max_L, flags=args.flags, stream=gs,
-                                    stream2=gs2)
+            case.step(0, stream=gs, stream2=gs2)
         for _ in range(3):
             cg.replay()
         torch.cuda.synchronize()
@@ -367,13 +537,15 @@ def main():
         gms = torch.tensor([g0.elapsed_time(g1) / K], device=dev)
         if world > 1:
             dist.all_reduce(gms, op=dist.ReduceOp.MAX)
-        ref_out = out.clone()
-        out.fill_(0)
+        ref_out = case.out.clone()
+        case.out.fill_(0)
         cg.replay()
         torch.cuda.synchronize()
-        same = bool(torch.equal(out, ref_out))
+        same = bool(torch.equal(case.out, ref_out))
         graph = {"ms_per_step": float(gms.item()), "value": tokens_all / (float(gms.item()) * 1e-3),
-                 "replay_matches_eager": same}
+                 "replay_matches_eager": same,
+                 "note": "replicas not rotated (one captured call)" if case.replicas > 1 else None}
+        del cg
     except Exception as ex:  # reported, never fatal
         graph = {"error": str(ex)[:200]}
 
@@ -389,32 +561,33 @@ def main():
     # duplex).  Every step still copies its whole q + metadata in and its whole out back.
     e2e = None
     if not args.no_e2e:
+        vc = inp["v_cache"]
         q_h = q.cpu().pin_memory()
         outs_h = [torch.empty_like(q_h).pin_memory() for _ in range(2)]
         out_h = outs_h[0]
         bt_h, cu_h, sl_h = (inp["block_table_h"].pin_memory(), inp["cu_seqlens_q_h"].pin_memory(),
                             inp["seq_lens_h"].pin_memory())
-        hp = pattn.make_problem(q_h, kc, w.num_kv_heads, w.block_size, bt_h, w.num_seqs, out_h, "NHD", max_q, max_L,
-                                args.flags)
+        hp = pattn.make_problem(q_h, kc, w.num_kv_heads, w.block_size, bt_h, w.num_seqs, out_h, "NHD", case.max_q,
+                                case.max_L, args.flags)
         hws = [torch.empty(pattn.hostio_workspace_size(hp), dtype=torch.uint8, device=dev) for _ in range(2)]
-        hst = [stream, torch.cuda.Stream(dev)]
+        hst = [case.stream, torch.cuda.Stream(dev)]
 
         def step_h(i):
             pattn.unified_attention_hostio(q_h, kc, vc, bt_h, cu_h, sl_h, w.scale, w.num_kv_heads, w.block_size,
-                                           outs_h[i % 2], max_query_len=max_q, max_seq_len=max_L, flags=args.flags,
-                                           workspace=hws[i % 2], stream=hst[i % 2])
+                                           outs_h[i % 2], max_query_len=case.max_q, max_seq_len=case.max_L,
+                                           flags=args.flags, workspace=hws[i % 2], stream=hst[i % 2])
 
         for i in range(4):
             step_h(i)
         torch.cuda.synchronize()
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        hst[1].wait_stream(stream)
+        e0.record(case.stream)
+        hst[1].wait_stream(case.stream)
         for i in range(K):
             step_h(i)
-        stream.wait_stream(hst[1])
-        e1.record(stream)
+        case.stream.wait_stream(hst[1])
+        e1.record(case.stream)
         torch.cuda.synchronize()
         barrier()
         ems = torch.tensor([e0.elapsed_time(e1) / K], device=dev)
@@ -425,46 +598,47 @@ def main():
         d2h = out_h.numel() * esz
         e2e = {"value": tokens_all / (float(ems.item()) * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": float(ems.item()), "requests_in_flight": 2}
+        del q_h, outs_h, hws
+
+    rl = roofline_of(case, ms, kern_ms, peaks, num_sms, load_traffic(args.workload))
+    dominant = max(rl.values(), key=lambda r: r["kernel_ms"]) if rl else None
+    kv_gb = kc.numel() * 2 * kc.element_size() / 1e9
+    work = kernel_work(w)
+    del case, inp, q, kc
+    torch.cuda.empty_cache()
+
+    # ---------------- keyed sub-results measured in the same run (north_star targets): config-4
+    # long-context decode and config-2 decode (K2 vs HBM), K1 alone on config 3's prefill half
+    # (serial, whole GPU, vs bf16), and config 5 as one global batch: on 1 GPU at N = 1, split
+    # by sequence and by KV head over the ranks (strong scaling, verified) at N > 1
+    subs = {}
+    if not args.no_sub and args.shard == "none" and not args.sim_world:
+        if world == 1:
+            Ks = min(K, 50)
+            for name, wl, st in (("c4_decode128k", CONFIGS["c4_decode128k"], 1),
+                                 ("c2_decode8b", CONFIGS["c2_decode8b"], 1),
+                                 ("c3p_prefill_part", ATTRIBUTION["c3p_prefill_part"], 1)):
+                if name == args.workload:
+                    continue
+                try:
+                    subs[name] = sub_result(name, wl, dev, pattn, st, Ks, args.warmup, peaks, num_sms, l2, barrier,
+                                            args.seed + 17)
+                except Exception as ex:  # reported, never fatal
+                    subs[name] = {"error": str(ex)[:200]}
+        try:
+            subs["c5_strong_scaling"] = strong_scaling_c5(args, dev, pattn, world, rank, barrier, l2)
+        except Exception as ex:
+            subs["c5_strong_scaling"] = {"error": str(ex)[:300]}
 
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return 0
 
-    peaks = load_peaks()
-    work = kernel_work(w)
-    num_sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    prefill_sms = prefill_sms_timed if pre_sms_known(kmask, pattn) else num_sms
-    sm_share = min(1.0, prefill_sms / num_sms)
-    rl = {}
-    pre_name = "prefill" if "prefill" in kern_ms else ("generic" if "generic" in kern_ms else None)
-    traffic = load_traffic(args.workload)
-    if pre_name and work["prefill_flops"] > 0:
-        t = kern_ms[pre_name] * 1e-3
-        a = work["prefill_flops"] / t / 1e12
-        # two streams: K1 runs on the P SMs K5 gave it (the decode kernel has the rest), so its
-        # tensor roof is the measured peak x P / #SMs; serial: P = all SMs
-        pk = peaks["bf16"] * sm_share
-        rl["prefill"] = {"bound": "tensor", "achieved": a, "peak": pk, "unit": "TFLOP/s",
-                         "frac": a / pk, "traffic": traffic.get(pre_name), "kernel": pre_name,
-                         "kernel_ms": kern_ms[pre_name], "share_of_step": kern_ms[pre_name] / ms,
-                         "prefill_sms": prefill_sms, "num_sms": num_sms}
-    if "decode" in kern_ms and work["decode_bytes"] > 0:
-        t = kern_ms["decode"] * 1e-3
-        a = work["decode_bytes"] / t / 1e9
-        rl["decode"] = {"bound": "hbm", "achieved": a, "peak": peaks["hbm"], "unit": "GB/s",
-                        "frac": a / peaks["hbm"], "traffic": traffic.get("decode"), "kernel": "decode",
-                        "kernel_ms": kern_ms["decode"], "share_of_step": kern_ms["decode"] / ms}
-    if "baseline" in kern_ms:  # the paper's App. A kernel (--flags 16): SIMT, reported by time only
-        rl["baseline"] = {"bound": "alu", "achieved": work["total_flops"] / (kern_ms["baseline"] * 1e-3) / 1e12,
-                          "peak": None, "unit": "TFLOP/s", "frac": None, "traffic": None, "kernel": "baseline",
-                          "kernel_ms": kern_ms["baseline"], "share_of_step": kern_ms["baseline"] / ms}
-    dominant = max(rl.values(), key=lambda r: r["kernel_ms"]) if rl else None
-
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         try:
-            cpu = cpu_baseline(w, inp)
+            cpu = cpu_baseline(w, args.seed + rank, dev)
         except Exception as ex:  # reported, never fatal
             cpu = {"value": None, "unit": "tokens/s", "cores": len(os.sched_getaffinity(0)), "kind": "oracle",
                    "sample": f"failed: {ex}"}
@@ -484,17 +658,18 @@ def main():
         "data": "synthetic",
         "config": {
             "workload": args.workload,
-            "seqs": f"{sum(1 for _, q in w.seqs if q > 1)} prefill x {max_q} tok + "
+            "seqs": f"{sum(1 for _, q in w.seqs if q > 1)} prefill x {max(qq for _, qq in w.seqs)} tok + "
                     f"{sum(1 for _, q in w.seqs if q == 1)} decode @ ctx {max((c for c, q in w.seqs if q == 1), default=0)}",
             "heads": f"{w.num_q_heads}q/{w.num_kv_heads}kv x d{w.head_dim}",
             "block_size": w.block_size,
             "tokens_per_step_per_gpu": w.num_tokens,
             "parallelism": parallelism_text(args, world, w_global, w),
             **({"comm_backend_test_only": backend} if backend != "nccl" else {}),
-            "l2": "inputs > L2 (KV cache %.2f GB/GPU), no flush" % (kc.numel() * 2 * kc.element_size() / 1e9),
+            "l2": "inputs > L2 (KV cache %.2f GB/GPU), no flush" % kv_gb,
             "streams": args.streams,
             "flags": args.flags,
-            "peaks": peaks["src"],
+            "peaks": peaks["src"] + " (MEASURED_PEAKS.json: HBM %.1f GB/s copy, bf16 %.1f TFLOP/s burst)"
+                     % (peaks["hbm"], peaks["bf16"]),
         },
         "roofline": ({k: dominant[k] for k in ("bound", "achieved", "peak", "unit", "frac", "traffic")}
                      if dominant else None),
@@ -505,6 +680,7 @@ def main():
         "cuda_graph": graph,
         "gpu_launches": launches_per_step * K,
         "cpu_baseline": cpu,
+        "sub_results": subs,
         "algorithmic": {"prefill_tflop_per_step": work["prefill_flops"] / 1e12,
                         "decode_gb_per_step": work["decode_bytes"] / 1e9,
                         "step_tflops": work["total_flops"] / (ms * 1e-3) / 1e12,
@@ -514,10 +690,6 @@ def main():
     if world > 1:
         dist.destroy_process_group()
     return 0
-
-
-def pre_sms_known(kmask, pattn):
-    return bool(kmask & (1 << pattn.KERNEL_PREFILL))
 
 
 def local_workload(w, mode, world, rank):

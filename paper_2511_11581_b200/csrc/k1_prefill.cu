@@ -80,16 +80,7 @@ constexpr int kHalfM = 128;    // rows per half (one UMMA M)
 constexpr int kM = 2 * kHalfM; // BLOCK_M
 constexpr int kN = 64;         // keys per KV tile
 constexpr int kD = 128;        // head dim
-// Column split (experiment): 8 more softmax warps (16-23, "part B") take key columns 32-63 of
-// every 64-key tile of their half; part A (warps 4-11) keeps columns 0-31 and all O work.
-// Row maxima are exchanged per tile through shared memory (16-bit, rounded up) between the
-// two warps of a TMEM lane quadrant; B's row sum is handed to A at the end of the item.
-#ifndef PATTN_K1_COLSPLIT
-#define PATTN_K1_COLSPLIT 0
-#endif
-constexpr bool kColSplit = PATTN_K1_COLSPLIT != 0;
-constexpr int kThreads = kColSplit ? 768 : 512;  // 24 / 16 warps
-constexpr int kNc = kColSplit ? 32 : 64;         // key columns per softmax warp
+constexpr int kThreads = 512;  // 16 warps
 // setmaxnreg budgets (16-warp layout): warpgroup 0 (producers, MMA a), warpgroups 1-2
 // (softmax), warpgroup 3 (V producer, scheduler, Q producer, MMA b); 128 (a + d) + 256 s = 65536
 #ifndef PATTN_K1_REG_WG0
@@ -102,7 +93,7 @@ constexpr int kNc = kColSplit ? 32 : 64;         // key columns per softmax warp
 #define PATTN_K1_REG_WG3 40
 #endif
 constexpr int kRegWG0 = PATTN_K1_REG_WG0, kRegSoftmax = PATTN_K1_REG_SOFTMAX, kRegWG3 = PATTN_K1_REG_WG3;
-static_assert(kColSplit || 128 * (kRegWG0 + kRegWG3) + 256 * kRegSoftmax <= 65536, "register budget");
+static_assert(128 * (kRegWG0 + kRegWG3) + 256 * kRegSoftmax <= 65536, "register budget");
 constexpr uint32_t kQTile = kHalfM * kD * 2;  // 32 KB: one 128-row half of the Q block
 constexpr uint32_t kHalf = kQTile / 2;         // 16 KB: one 64-wide d half of it
 constexpr uint32_t kTile = kN * kD * 2;        // 16 KB: one K or V tile (64 keys)
@@ -117,31 +108,13 @@ constexpr uint32_t kSub16Bytes = 16 * kD * 2;  // 4 KB: one 16-key sub-block of 
 #endif
 constexpr int kKStages = PATTN_K1_KST;
 constexpr int kVStages = PATTN_K1_VST;  // V waits on PV (later than S), so it gets the deeper ring
-// Exponential-phase ping-pong between the two softmax warpgroups (named barriers 1, 2): the
-// halves' S tiles complete ~one UMMA apart, so without it both warpgroups hit MUFU.EX2 at the
-// same time (the pipe is saturated for ~half a tile period and idle for the rest: trace
-// "max->exp" 1276 clk of a ~2400 clk period).  With it, WG a's exponentials of tile j run
-// while WG b does its load / max / P store, and vice versa.
-#ifndef PATTN_K1_PINGPONG
-#define PATTN_K1_PINGPONG 0  // measured slower: off
+#ifndef PATTN_K1_TRUNC
+#define PATTN_K1_TRUNC 0
 #endif
-constexpr int kBarExpA = 1, kBarExpB = 2;
-// Load the next tile's S from TMEM as soon as the current tile's exponentials are done, when
-// it is already complete (non-blocking test), instead of after this tile's P store.
-#ifndef PATTN_K1_SPREFETCH
-#define PATTN_K1_SPREFETCH 0  // measured: 791 vs 939 TFLOP/s (register spills), off
+#ifndef PATTN_K1_PP
+#define PATTN_K1_PP 0
 #endif
-// P -> bf16 with integer ops (round half up on the fp32 bits, then a byte permute) instead of
-// F2FP: F2FP issues on the same XU pipe as MUFU.EX2 (measured 8 clk per warp instruction per
-// SMSP for both, scripts/micro/pipes.cu), i.e. one third of the softmax's XU time.
-#ifndef PATTN_K1_ALU_PACK
-#define PATTN_K1_ALU_PACK 0  // measured slower: off
-#endif  // "half a may start its exponentials" / "half b may"
 constexpr float kRescaleThreshold = 8.0f;  // log2 domain: rescale O only if the max grows by > 2^8
-#ifndef PATTN_POLY_MASK
-#define PATTN_POLY_MASK 255  // measured: FMA-pipe exp2 did not pay off here
-#endif
-constexpr int kPolyMask = PATTN_POLY_MASK;  // exp2 pair j on the FMA pipe iff (j & mask) == mask: 1 -> 1/2
 
 // shared-memory map (offsets from a 1024-aligned base)
 constexpr uint32_t kOffQ = 0;  // half a: [0, 32K), half b: [32K, 64K)
@@ -149,17 +122,12 @@ constexpr uint32_t kOffK = kOffQ + 2 * kQTile;
 constexpr uint32_t kOffV = kOffK + kKStages * kTile;
 // epilogue staging: per half 16 KB = 4 warps x 32 rows x 128 B (one 64-wide d half at a time),
 // 128B-swizzled as the out TMA map expects
-#ifndef PATTN_K1_STAGE_FULL
-#define PATTN_K1_STAGE_FULL 1  // 8 KB per warp: both d halves at once, no read wait in between
-                               // (measured +2.7% over 4 KB with K/V rings 4/4)
-#endif
-constexpr uint32_t kStageWarp = PATTN_K1_STAGE_FULL ? 8192 : 4096;
+constexpr uint32_t kStageWarp = 8192;  // both 64-wide d halves staged at once (no read wait in between)
 constexpr uint32_t kStageHalf = 4 * kStageWarp;
 constexpr uint32_t kOffStage = kOffV + kVStages * kTile;
 constexpr uint32_t kOffBar = kOffStage + 2 * kStageHalf;
 constexpr uint32_t kBarBlock = 512;  // barriers + the item ring
-constexpr uint32_t kOffX = kOffBar + kBarBlock;  // column-split exchange: 16-bit maxima / fp32 row sums
-constexpr uint32_t kSmemBytes = kOffX + (kColSplit ? 1024 : 0) + 1024;
+constexpr uint32_t kSmemBytes = kOffBar + kBarBlock + 1024;
 static_assert(kSmemBytes <= 227 * 1024, "shared memory budget");
 
 // TMEM columns
@@ -186,14 +154,8 @@ struct Bars {
 
 // One MMA-issuing warp per half (warp 1: half a, warp 15: half b) so that one half's chain
 // S(j) -> softmax(j) -> PV(j) never waits behind the other half's softmax.
-#ifndef PATTN_K1_SPLIT_MMA
-#define PATTN_K1_SPLIT_MMA 1
-#endif
-constexpr int kMmaWarps = PATTN_K1_SPLIT_MMA ? 2 : 1;
-#ifndef PATTN_K1_SKEW_CLK
-#define PATTN_K1_SKEW_CLK 0
-#endif
-constexpr int kItemConsumers = 14 + (kMmaWarps - 1) + (kColSplit ? 8 : 0);  // warps 0-3, 12, 14, (15) and the 8 softmax warps
+constexpr int kMmaWarps = 2;
+constexpr int kItemConsumers = 15;  // warps 0-3, 12, 14, 15 and the 8 softmax warps
 
 struct Item {
   int b, kvh, q0, qlen, L, ctx, tok0, ntok, kv_end, ntiles;
@@ -224,44 +186,6 @@ __device__ __forceinline__ Item prefill_item(const Params& p, int total_qb, int 
   x.kv_end = x.ctx + x.tok0 + x.ntok;  // keys visible to the Q block's last row
   x.ntiles = (x.kv_end + kN - 1) / kN;
   return x;
-}
-
-// The XU pipe (MUFU.EX2 and F2FP conversions) is the softmax's bottleneck on B200: per
-// 128x128 tile, 16384 exp2 + 8192 bf16x2 packs at 8 ops/clk/SM take ~3x the 1024 clk the
-// two UMMAs need.  So (1) P is packed to bf16 with integer ops (round-half-up on the fp32
-// bits, then a byte permute) and (2) a fraction of the exp2 run on the FMA pipe:
-// 2^x = 2^n * p(f), n = rint(x), f = x - n in [-0.5, 0.5], p a degree-3 minimax polynomial
-// (max relative error 7.5e-5, far below bf16's 2^-9 rounding of P; reading R12).
-PATTN_DEVICE uint32_t pack_bf16_alu(float lo, float hi) {
-  const uint32_t a = __float_as_uint(lo) + 0x8000u, b = __float_as_uint(hi) + 0x8000u;
-  return __byte_perm(a, b, 0x7632);  // {hi16(b), hi16(a)}; p >= 0 and finite
-}
-PATTN_DEVICE float exp2_poly(float x) {
-  x = fmaxf(x, -126.f);                          // keeps 2^n a normal power of two (tiny, not 0)
-  const float t = __fadd_rn(x, 12582912.f);      // 1.5 * 2^23: n = rint(x) in the low mantissa bits
-  const float n = __fadd_rn(t, -12582912.f);
-  const float f = __fadd_rn(x, -n);
-  float pp = fmaf(0.05500858277082443f, f, 0.24221037328243256f);
-  pp = fmaf(pp, f, 0.6932829022407532f);
-  pp = fmaf(pp, f, 1.0f);
-  return __int_as_float(__float_as_int(pp) + (__float_as_int(t) << 23));
-}
-
-// Packed form on the FMA pipe (FADD2/FFMA2) for a pair of exponents; x <= 0 or -inf.
-PATTN_DEVICE uint64_t exp2_poly2(uint64_t xx) {
-  const float x0 = fmaxf(f32x2_lo(xx), -127.f), x1 = fmaxf(f32x2_hi(xx), -127.f);
-  const uint64_t x = f32x2(x0, x1);
-  const uint64_t t = fadd2(x, f32x2(12582912.f, 12582912.f));  // n = rint(x) in the low mantissa bits
-  const uint64_t n = fadd2(t, f32x2(-12582912.f, -12582912.f));
-  const uint64_t f = fadd2(x, n ^ 0x8000000080000000ull);       // x - n in [-0.5, 0.5]
-  // p(f) = 1 + c1 f + c2 f^2 + c3 f^3, relative-minimax on [-0.5, 0.5] with p(0) = 1 exactly
-  // (so a lone maximum gets exactly P = 1, like ex2.approx), max relative error 1.0e-4
-  uint64_t pp = ffma2(f32x2(0.05500858277082443f, 0.05500858277082443f), f,
-                      f32x2(0.24221037328243256f, 0.24221037328243256f));
-  pp = ffma2(pp, f, f32x2(0.6932829022407532f, 0.6932829022407532f));
-  pp = ffma2(pp, f, f32x2(1.0f, 1.0f));
-  const uint32_t lo = (uint32_t)pp + ((uint32_t)t << 23), hi = (uint32_t)(pp >> 32) + ((uint32_t)(t >> 32) << 23);
-  return (uint64_t)lo | ((uint64_t)hi << 32);
 }
 
 // O[tmem] (+)= A[tmem] * B[smem desc]; kind::f16, A (P) K-major in TMEM.
@@ -328,7 +252,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int h = 0; h < 2; ++h) {
       mbar_init(&bar.s_full[h][0], 1);
       mbar_init(&bar.s_full[h][1], 1);
-      mbar_init(&bar.p_full[h], kColSplit ? 2 * kHalfM : kHalfM);
+      mbar_init(&bar.p_full[h], kHalfM);
       mbar_init(&bar.pv_done[h], 1);
       mbar_init(&bar.o_empty[h], kHalfM);
     }
@@ -409,7 +333,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ++cnt;
       }
     }
-  } else if (warp == 1 || (PATTN_K1_SPLIT_MMA && warp == 15)) {
+  } else if (warp == 1 || warp == 15) {
     // ================================================================ MMA issuer(s)
     // The whole warp runs the schedule (waits, descriptor arithmetic stay warp-uniform, in
     // uniform registers); one elected lane issues each tcgen05.mma / commit.  With two MMA
@@ -419,8 +343,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kRegWG0) : "memory");
     else
       asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kRegWG3) : "memory");  // warpgroup 3
-    const int h_lo = (PATTN_K1_SPLIT_MMA && warp == 15) ? 1 : 0;
-    const int h_hi = PATTN_K1_SPLIT_MMA ? h_lo + 1 : 2;
+    const int h_lo = warp == 15 ? 1 : 0;
+    const int h_hi = h_lo + 1;
     constexpr uint32_t idS = idesc_bf16_f32(kHalfM, kN, 0, 0);   // Q (K-major) x K (K-major)
     constexpr uint32_t idPV = idesc_bf16_f32(kHalfM, kD, 0, 1);  // P (TMEM, K-major) x V (MN-major)
     // smem descriptors: start-address field = addr >> 4, so desc(base + off) = desc(base) + (off >> 4)
@@ -435,13 +359,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (x.ntiles < 0) break;
       if (leader) PATTN_K1_TRACE(40);
       mbar_wait(&bar.q_full, ic & 1u);
-#if PATTN_K1_SKEW_CLK > 0
-      if (h_lo == 1) {  // experiment: start half b's chain late so the halves' exp phases interleave
-        const long long t_end = clock64() + PATTN_K1_SKEW_CLK;
-        while (clock64() < t_end) {
-        }
-      }
-#endif
       if (leader) PATTN_K1_TRACE(41);
       tc_fence_after();
       // Iteration jt: S_a(jt), S_b(jt) into S buffer jt&1 of each half, then PV_a(jt-1),
@@ -463,9 +380,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int k = 0; k < kD / 16; ++k) {
                 const uint32_t offq = ((k >> 2) * kHalf + (k & 3) * 32) >> 4;
                 const uint32_t offk = ((k >> 2) * 1024 + (k & 3) * 32) >> 4;
-#ifndef PATTN_K1_NOMMA  // timing experiment only: no tensor work
                 tc_mma_f16_ss(tS, dq + offq, dk + offk, idS, k > 0 ? 1u : 0u);
-#endif
               }
               PATTN_K1_TRACE(7 + h);
               tc_commit(&bar.s_full[h][jt & 1]);
@@ -490,9 +405,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               const uint64_t dv = dV + ((vs * kTile) >> 4);
 #pragma unroll
               for (int k = 0; k < kN / 16; ++k) {
-#ifndef PATTN_K1_NOMMA
                 tc_mma_f16_ts(tO, tP + 8 * k, dv + ((k * kSub16Bytes) >> 4), idPV, (jt > 1 || k > 0) ? 1u : 0u);
-#endif
               }
               PATTN_K1_TRACE(5 + h);
               tc_commit(&bar.pv_done[h]);
@@ -571,17 +484,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ================================================================ softmax / correction / epilogue
-    if constexpr (kColSplit)
-      asm volatile("setmaxnreg.inc.sync.aligned.u32 96;\n" ::: "memory");  // 128*56 + 128*40 + 512*96 = 80*768
-    else
-      asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kRegSoftmax) : "memory");
-    const int part = (kColSplit && warp >= 16) ? 1 : 0;      // key columns [32 part, +kNc)
-    const int h = part ? (warp - 16) >> 2 : (warp - 4) >> 2;  // half a (0) or b (1)
-    const int r = 32 * (warp & 3) + lane;                      // row within the half == TMEM lane
-    const int colb = part * kNc;
-    const int xbar = 3 + h * 4 + (warp & 3);  // named barrier of the (A, B) warp pair (column split)
-    uint16_t* xs = reinterpret_cast<uint16_t*>(smem + kOffX);
-    float* xf = reinterpret_cast<float*>(smem + kOffX);
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kRegSoftmax) : "memory");
+    const int h = (warp - 4) >> 2;        // half a (0) or b (1)
+    const int r = 32 * (warp & 3) + lane;  // row within the half == TMEM lane
     const uint32_t lane_off = (uint32_t)(32 * (warp & 3)) << 16;
     const uint32_t tS0 = tmem + kTmemS + 128 * h + lane_off;
     const uint32_t tO = tmem + kTmemO + 128 * h + lane_off;
@@ -592,7 +497,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float cs = p.scale_log2;
     const float ca = fmaxf(fabsf(cs), 1e-30f);  // scale 0: -inf * 0 would be NaN; 1e-30 * s ~ 0
     uint32_t ic = 0;
-    if (PATTN_K1_PINGPONG && h == 1) named_bar_arrive(kBarExpA, 2 * kHalfM);  // half a goes first
+    if (PATTN_K1_PP && h == 1) named_bar_arrive(1, 256);  // half a goes first
     for (;; ++ic) {
       const Item x = next_item(bar, ring, ic, lane);
       if (x.ntiles < 0) break;
@@ -601,73 +506,39 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int row_lim = min(x.ctx + x.tok0 + tk + 1, x.kv_end);  // keys [0, row_lim) visible
       const int nsb_valid = (x.kv_end + 15) / 16;                  // 16-key sub-blocks fetched
       float m_run = -INFINITY, l_run = 0.f;
-      float s[kNc];
-      bool s_loaded = false;  // S of this tile already requested by the previous iteration
+      float s[kN];
       for (int jt = 0; jt < x.ntiles; ++jt) {
         const int sb = jt & 1;  // S buffer of this tile (P is written back over it)
         const uint32_t tS = tS0 + 64 * sb;
-        if (!s_loaded) {
-          mbar_wait(&bar.s_full[h][sb], (sb ? sc1 : sc0) & 1u);
-          sc0 += sb ? 0u : 1u;
-          sc1 += sb ? 1u : 0u;
-        }
+        mbar_wait(&bar.s_full[h][sb], (sb ? sc1 : sc0) & 1u);
+        sc0 += sb ? 0u : 1u;
+        sc1 += sb ? 1u : 0u;
         if (r == 0) PATTN_K1_TRACE(10 + h);
         tc_fence_after();
-#ifdef PATTN_K1_NOSOFTMAX  // timing experiment only: P = bf16 pairs of S, no max / exp / rescale
-        {
-          uint32_t pz[32];
-          PATTN_TMEM_LD32(tS + 0, pz);
-          tmem_wait_ld();
-          PATTN_TMEM_ST32(tS + 0, pz);
-          ++vc;
-          tmem_wait_st();
-          tc_fence_before();
-          mbar_arrive(&bar.p_full[h]);
-          ++tc;
-          l_run = 1.f;
-          if (jt > 0) mbar_wait(&bar.pv_done[h], (tc - 2) & 1u);
-          continue;
-        }
-#endif
         {
           uint32_t* su = reinterpret_cast<uint32_t*>(s);
-          if (!s_loaded) {
-            PATTN_TMEM_LD32(tS + colb, (su + 0));
-            if constexpr (kNc == 64) PATTN_TMEM_LD32(tS + 32, (su + 32));
-          }
+          PATTN_TMEM_LD32(tS + 0, (su + 0));
+          PATTN_TMEM_LD32(tS + 32, (su + 32));
           tmem_wait_ld();
         }
-        s_loaded = false;
         if (r == 0) PATTN_K1_TRACE(30 + h);
         const int key0 = jt * kN;
         const int nvis = row_lim - key0;  // keys [key0, key0 + nvis) of this tile are visible
         if (cs < 0.f) {  // sign-adjust so that max(raw) * |c| = max(scaled)
 #pragma unroll
-          for (int c = 0; c < kNc; ++c) s[c] = -s[c];
+          for (int c = 0; c < kN; ++c) s[c] = -s[c];
         }
-        if (__any_sync(0xffffffffu, nvis < colb + kNc)) {  // diagonal / tail tile: causal mask (warp-uniform)
+        if (__any_sync(0xffffffffu, nvis < kN)) {  // diagonal / tail tile: causal mask (warp-uniform)
 #pragma unroll
-          for (int c = 0; c < kNc; ++c) s[c] = c + colb < nvis ? s[c] : -INFINITY;
+          for (int c = 0; c < kN; ++c) s[c] = c < nvis ? s[c] : -INFINITY;
         }
         float mx[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) mx[i] = s[i];
 #pragma unroll
-        for (int c = 8; c < kNc; ++c) mx[c & 7] = fmaxf(mx[c & 7], s[c]);
-        float mraw = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
-                           fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
-        if constexpr (kColSplit) {
-          // both warps of the pair must use the same row max: exchange 16-bit values rounded
-          // toward +inf (any upper bound of the row max is a valid shift) and take the max
-          uint32_t u = __float_as_uint(mraw);
-          u = (int32_t)u >= 0 && (u & 0xffffu) ? u + 0x10000u : u;
-          const uint16_t mine = (uint16_t)(u >> 16);
-          named_bar_sync(xbar, 64);  // the partner has read the previous value
-          xs[(h * 2 + part) * kHalfM + r] = mine;
-          named_bar_sync(xbar, 64);
-          const uint16_t other = xs[(h * 2 + (part ^ 1)) * kHalfM + r];
-          mraw = fmaxf(__uint_as_float((uint32_t)mine << 16), __uint_as_float((uint32_t)other << 16));
-        }
+        for (int c = 8; c < kN; ++c) mx[c & 7] = fmaxf(mx[c & 7], s[c]);
+        const float mraw = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                                 fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
         if (r == 0) PATTN_K1_TRACE(32 + h);
         const float mt = mraw * ca;
         const float m_new = fmaxf(m_run, mt);
@@ -681,60 +552,34 @@ __global__ void __launch_bounds__(kThreads, 1)
         // exponent argument and the row sum
         const uint64_t ca2 = f32x2(ca, ca), nb2 = f32x2(nbase, nbase);
         uint64_t rs2[4] = {0ull, 0ull, 0ull, 0ull};
-        uint32_t pk[kNc / 2];
-        // both halves see the same number of tiles per item, so the turns strictly alternate
-        if (PATTN_K1_PINGPONG) named_bar_sync(h ? kBarExpB : kBarExpA, 2 * kHalfM);
+        uint32_t pk[kN / 2];
+        if (PATTN_K1_PP) named_bar_sync(h ? 2 : 1, 256);
 #pragma unroll
-        for (int c = 0; c < kNc; c += 2) {
+        for (int c = 0; c < kN; c += 2) {
           // e^{scale*qk - m} in the log2 domain
           const uint64_t xx = ffma2(f32x2(s[c], s[c + 1]), ca2, nb2);
-          uint64_t ee;
-          float e0, e1;
-          if ((((c >> 1) & kPolyMask) == kPolyMask) && kPolyMask < 64) {  // this pair on the FMA pipe
-            ee = exp2_poly2(xx);
-            e0 = f32x2_lo(ee);
-            e1 = f32x2_hi(ee);
-          } else {
-            e0 = fast_exp2(f32x2_lo(xx));
-            e1 = fast_exp2(f32x2_hi(xx));
-            ee = f32x2(e0, e1);
-          }
-          rs2[(c >> 1) & 3] = fadd2(rs2[(c >> 1) & 3], ee);
-#if PATTN_K1_ALU_PACK
-          pk[c >> 1] = pack_bf16_alu(e0, e1);  // ALU pipe: keeps the XU pipe for MUFU.EX2
+          const float e0 = fast_exp2(f32x2_lo(xx)), e1 = fast_exp2(f32x2_hi(xx));
+          rs2[(c >> 1) & 3] = fadd2(rs2[(c >> 1) & 3], f32x2(e0, e1));
+#if PATTN_K1_TRUNC
+          pk[c >> 1] = __byte_perm(__float_as_uint(e0), __float_as_uint(e1), 0x7632);
 #else
-          pk[c >> 1] = pack_bf16(e0, e1);  // F2FP: shares the XU pipe with MUFU.EX2
+          pk[c >> 1] = pack_bf16(e0, e1);
 #endif
         }
-        if (PATTN_K1_PINGPONG) named_bar_arrive(h ? kBarExpA : kBarExpB, 2 * kHalfM);
-#if PATTN_K1_SPREFETCH
-        // s[] is dead now: if the next tile's S is already complete, request it from TMEM so
-        // that its load latency hides behind this tile's PV wait, rescale and P store (the
-        // test is made warp-uniform: tcgen05.ld is warp-collective)
-        if (jt + 1 < x.ntiles) {
-          const int nb = (jt + 1) & 1;
-          const bool ready = __all_sync(0xffffffffu, mbar_test(&bar.s_full[h][nb], (nb ? sc1 : sc0) & 1u));
-          if (ready) {
-            sc0 += nb ? 0u : 1u;
-            sc1 += nb ? 1u : 0u;
-            tc_fence_after();
-            uint32_t* su = reinterpret_cast<uint32_t*>(s);
-            PATTN_TMEM_LD32(tS0 + 64 * nb + 0, (su + 0));
-            PATTN_TMEM_LD32(tS0 + 64 * nb + 32, (su + 32));
-            s_loaded = true;
-          }
-        }
-#endif
+        if (PATTN_K1_PP) named_bar_arrive(h ? 1 : 2, 256);
         const uint64_t r01 = fadd2(rs2[0], rs2[1]), r23 = fadd2(rs2[2], rs2[3]), rr = fadd2(r01, r23);
         const float rs = f32x2_lo(rr) + f32x2_hi(rr);
         if (r == 0) PATTN_K1_TRACE(34 + h);
         // O_h: PV_h(jt-1) (issued once P_h(jt-1) arrived, while this tile's exponentials ran)
         // must be complete before O_h is corrected and before P_h(jt) can be consumed.
-        if (part == 0 && jt > 0) {
+        const bool need_rescale = __any_sync(0xffffffffu, alpha != 1.f);
+        // (the wait cannot be skipped when no row rescales: mbarrier parity only tells phases
+        // apart one step back, so every pv_done phase must be observed in order)
+        if (jt > 0) {
           mbar_wait(&bar.pv_done[h], (tc - 1) & 1u);
           tc_fence_after();
           // tcgen05.ld/st are warp-collective (.sync.aligned): rescale when ANY row of the warp needs it
-          if (__any_sync(0xffffffffu, alpha != 1.f)) {
+          if (need_rescale) {
 #pragma unroll
             for (int c0 = 0; c0 < kD; c0 += 32) {
               uint32_t o[32];
@@ -749,14 +594,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         l_run = l_run * alpha + rs;
         m_run = m_use;
         // P (bf16, 2 per column) over the first 32 columns of the S buffer: the A operand of PV_h
-        if constexpr (kColSplit)
-          PATTN_TMEM_ST16(tS + part * 16, (pk + 0));
-        else
-          PATTN_TMEM_ST32(tS + 0, (pk + 0));
-        // Zero V rows of slots >= L inside the last fetched sub-block (they may hold NaN).  With
-        // one MMA warp, WG a does it (PV_b is issued after PV_a); with one MMA warp per half
-        // each WG does it before releasing its own P (both write the same zeros).
-        if ((h == 0 || PATTN_K1_SPLIT_MMA) && part == 0) {
+        PATTN_TMEM_ST32(tS + 0, (pk + 0));
+        // Zero V rows of slots >= L inside the last fetched sub-block (they may hold NaN); each
+        // warpgroup does it before releasing its own P (both write the same zeros).
+        {
           const int z0 = x.L - key0, z1 = min(kN, nsb_valid * 16 - key0);
           if (z0 < z1 && z0 < kN) {
             const uint32_t s2 = vc % kVStages;
@@ -776,13 +617,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (r == 0) PATTN_K1_TRACE(12 + h);
         mbar_arrive(&bar.p_full[h]);
         ++tc;
-      }
-      if constexpr (kColSplit) {  // B hands its partial row sum to A, which does the epilogue
-        named_bar_sync(xbar, 64);   // A has read B's last row max
-        if (part == 1) xf[h * kHalfM + r] = l_run;
-        named_bar_sync(xbar, 64);
-        if (part == 1) continue;
-        l_run += xf[h * kHalfM + r];
       }
       // ---- epilogue: O / l -> bf16 -> out (valid rows only)
       mbar_wait(&bar.pv_done[h], (tc - 1) & 1u);
@@ -813,8 +647,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int tok_w = x.q0 + x.tok0 + h * bq_half + (r & ~31) / G;
 #pragma unroll
         for (int pass = 0; pass < 2; ++pass) {
-          uint8_t* stg = stg0 + (PATTN_K1_STAGE_FULL ? pass * 4096 : 0);
-          if (pass == 0 || !PATTN_K1_STAGE_FULL) {
+          uint8_t* stg = stg0 + pass * 4096;
+          if (pass == 0) {
             if (lane == 0) bulk_wait_group_read0();  // the slice's previous store has read it
             __syncwarp();
           }
@@ -858,8 +692,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (r == 0) PATTN_K1_TRACE(44 + h);
     }
     if (lane == 0) bulk_wait_group0();  // epilogue stores complete before the CTA retires
-    // drain half b's last hand-over (its final arrive on kBarExpA has no partner otherwise)
-    if (PATTN_K1_PINGPONG && h == 0) named_bar_sync(kBarExpA, 2 * kHalfM);
+    if (PATTN_K1_PP && h == 0) named_bar_sync(1, 256);  // drain half b's last hand-over
     if (threadIdx.x == 128) PATTN_CTA_END(k1, ic);
   }
 
@@ -890,7 +723,7 @@ PrefillLaunch plan_prefill(const Params& p, int num_sms) {
 
 cudaError_t launch_prefill(const Params& p, const PrefillLaunch& pl, const CUtensorMap& tmQ, const CUtensorMap& tmO,
                            const KvHeadMaps& kv, cudaStream_t stream) {
-  cudaError_t e = cudaFuncSetAttribute(k1_prefill, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
+  cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(k1_prefill), pl.smem);
   if (e != cudaSuccess) return e;
   k1_prefill<<<pl.grid, kThreads, pl.smem, stream>>>(tmQ, tmO, kv, p);
   return cudaGetLastError();

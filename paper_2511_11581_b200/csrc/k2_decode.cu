@@ -85,11 +85,7 @@ __device__ __forceinline__ Item decode_item(const Params& p, int it) {
   return x;
 }
 
-// PIPE: each consumer warp computes the scores S^T of its NEXT sub-block (j + NCW) before the
-// softmax and P.V of the current one, so the 8-deep dependent mma chain of QK^T overlaps the
-// current sub-block's shuffles, exponentials and PV mmas (needs nst >= 2 * NCW: the warp holds
-// two stages at once).
-template <int D, int NCW, bool PIPE>
+template <int D, int NCW>
 __global__ void __launch_bounds__((NCW + kNP) * 32, 1)
     k2_decode(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, Params p,
               int nst) {
@@ -254,21 +250,11 @@ __global__ void __launch_bounds__((NCW + kNP) * 32, 1)
         mma_bf16_16816(sc, a0, a1, a2, a3, bq[kc][0], bq[kc][1]);
       }
     };
-    float sc_next[4] = {0.f, 0.f, 0.f, 0.f};
-    if (PIPE && cw < nsb) scores(cw, sc_next);
     for (int j = cw; j < nsb; j += NCW) {
       const uint32_t gg = g + j;
       const uint32_t s = gg % nst;
       float sc[4];
-      if (PIPE) {
-        sc[0] = sc_next[0];
-        sc[1] = sc_next[1];
-        sc[2] = sc_next[2];
-        sc[3] = sc_next[3];
-        if (j + NCW < nsb) scores(j + NCW, sc_next);  // overlaps this sub-block's softmax / PV
-      } else {
-        scores(j, sc);
-      }
+      scores(j, sc);
       const uint32_t kst = ring_u32 + s * S::kStageBytes;
       const uint32_t vst = kst + S::kOpBytes;
       const int valid = x.L - (x.sb0 + j) * kSub;  // slots [0, valid) hold real keys
@@ -383,38 +369,6 @@ __global__ void __launch_bounds__((NCW + kNP) * 32, 1)
         }
       }
     }
-    if (p.fuse_reduce && x.nseg > 1) {
-      // Fused segment merge (the K3 step): the CTA that completes a unit's last
-      // segment merges all its partials, in segment order (deterministic whichever CTA is
-      // last).  Release: every writer fences, then one thread counts the segment in.
-      __threadfence();
-      named_bar_sync(1, NCW * 32);
-      volatile int* s_last = reinterpret_cast<volatile int*>(scratch);  // scratch is free again
-      if (ct == 0) {
-        const int unit = x.b * p.Hkv * p.HG + x.kvh * p.HG + x.hg;
-        const int done = atomicAdd(p.seg_cnt + unit, 1);
-        __threadfence();  // acquire: the other segments' partials are visible below
-        *s_last = (done == x.nseg - 1);
-      }
-      named_bar_sync(1, NCW * 32);
-      if (*s_last) {
-        const int cfirst = __ldg(p.cu_ch + x.b);  // first segment of the sequence
-        for (int idx = ct; idx < g_eff * D; idx += NCW * 32) {
-          const int h = idx / D, d = idx - h * D;
-          float M = -INFINITY;
-          for (int s = 0; s < x.nseg; ++s) M = fmaxf(M, __ldcg(p.part_m + (int64_t)(cfirst + s) * p.Hq + head0 + h));
-          float num = 0.f, den = 0.f;
-          for (int s = 0; s < x.nseg; ++s) {
-            const int64_t row = (int64_t)(cfirst + s) * p.Hq + head0 + h;
-            const float ms = __ldcg(p.part_m + row);
-            const float w = ms == -INFINITY ? 0.f : exp2f(ms - M);
-            den = fmaf(w, __ldcg(p.part_l + row), den);
-            num = fmaf(w, __ldcg(p.part_acc + row * D + d), num);
-          }
-          O[(int64_t)x.tok * p.o_st_tok + (int64_t)(head0 + h) * p.o_st_head + d] = __float2bfloat16_rn(num / den);
-        }
-      }
-    }
     named_bar_sync(1, NCW * 32);
     if (lane == 0 && cw == 0) PATTN_EV(k2, 5, ni);
   }
@@ -426,10 +380,8 @@ int env_or(const char* name, int dflt);
 template <int D, int NCW>
 cudaError_t launch_dw(const Params& p, const DecodeLaunch& dl, const CUtensorMap& tmK, const CUtensorMap& tmV,
                       cudaStream_t stream) {
-  // measured slower (config 2 167 -> 200 us, 36-SM decode 603 -> 993 us): opt-in only
-  const bool pipe = env_or("PATTN_K2_PIPE", 0) != 0 && dl.stages >= 2 * NCW;
-  auto kern = pipe ? k2_decode<D, NCW, true> : k2_decode<D, NCW, false>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dl.smem);
+  auto kern = k2_decode<D, NCW>;
+  cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(kern), dl.smem);
   if (e != cudaSuccess) return e;
   kern<<<dl.grid, (NCW + kNP) * 32, dl.smem, stream>>>(tmK, tmV, p, dl.stages);
   return cudaGetLastError();

@@ -16,43 +16,46 @@
 namespace pattn {
 namespace {
 
-// SG x 64 threads = SG segment groups x 8 heads x 8 float4 columns: thread (sg, h, d4) reduces
-// the segments s = sg (mod SG) of head h for columns 4*d4 .. 4*d4+3 of the CTA's 32-column
-// slice, then the groups are combined through shared memory in group order (deterministic).
-// SG = 4 for long contexts (config 4: 37 segments per unit; the reduce went 17 -> 11 us), SG = 1
-// when segments are few (config 2: 5 segments; four groups only added threads and barriers).
-template <int D, int kSegGroups>
-__global__ void __launch_bounds__(64 * kSegGroups) k3_reduce(Params p) {
-  __shared__ float s_max[kSegGroups][8];
-  __shared__ float4 s_num[kSegGroups][8][8];
-  __shared__ float s_den[kSegGroups][8];
+// 256 threads = 4 segment groups x 8 heads x 8 float4 columns: thread (sg, h, d4) reduces the
+// segments s = sg (mod SG) of head h for columns 4*d4 .. 4*d4+3 of the CTA's 32-column slice,
+// then the groups are combined through shared memory in group order (deterministic).  The
+// number of active groups SG = clamp(ceil(n / 8), 1, 4) follows the sequence's actual segment
+// count n (config 2: 5 segments -> 1 group; config 4: 37 -> 4); for a given n the order of
+// the additions is fixed, so the result is bitwise reproducible.
+constexpr int kMaxGroups = 4;
+
+template <int D>
+__global__ void __launch_bounds__(64 * kMaxGroups) k3_reduce(Params p) {
+  __shared__ float s_max[kMaxGroups][8];
+  __shared__ float4 s_num[kMaxGroups][8][8];
+  __shared__ float s_den[kMaxGroups][8];
   const int b = blockIdx.x;
   const int qb = p.cu_seqlens_q[b + 1] - p.cu_seqlens_q[b];
   if (!(p.decode_to_k2 && qb == 1)) return;
   const int c0 = p.cu_ch[b];
   const int n = p.cu_ch[b + 1] - c0;
   if (n <= 1) return;  // K2 wrote the final output itself
+  const int groups = min(kMaxGroups, (n + 7) / 8);
   const int kvh = blockIdx.y / p.HG, hg = blockIdx.y % p.HG;
   const int g_eff = min(8, p.G - hg * 8);
   const int head0 = kvh * p.G + hg * 8;
   const int tok = p.cu_seqlens_q[b];
   const int d4 = threadIdx.x & 7, h = (threadIdx.x >> 3) & 7, sg = threadIdx.x >> 6;
-  const bool active = h < g_eff;
+  const bool active = h < g_eff && sg < groups;
   const int d4g = blockIdx.z * 8 + d4;  // float4 column within the head
   // 1. M = max_s m_s per head (each group over its segments, then across groups)
   float M = -INFINITY;
   if (active)
-    for (int c = sg; c < n; c += kSegGroups) M = fmaxf(M, p.part_m[(int64_t)(c0 + c) * p.Hq + head0 + h]);
+    for (int c = sg; c < n; c += groups) M = fmaxf(M, p.part_m[(int64_t)(c0 + c) * p.Hq + head0 + h]);
   if (d4 == 0) s_max[sg][h] = M;
   __syncthreads();
-#pragma unroll
-  for (int g = 0; g < kSegGroups; ++g) M = fmaxf(M, s_max[g][h]);
+  for (int g = 0; g < groups; ++g) M = fmaxf(M, s_max[g][h]);
   // 2. w_s = 2^{m_s - M} (0 for an empty segment); num = sum w_s acc_s, den = sum w_s l_s
   float den = 0.f;
   float4 num = make_float4(0.f, 0.f, 0.f, 0.f);
   if (active) {
-#pragma unroll 4
-    for (int c = sg; c < n; c += kSegGroups) {
+#pragma unroll 8
+    for (int c = sg; c < n; c += groups) {
       const int64_t row = (int64_t)(c0 + c) * p.Hq + head0 + h;
       const float mc = p.part_m[row];
       const float w = (mc == -INFINITY) ? 0.f : exp2f(mc - M);
@@ -70,8 +73,7 @@ __global__ void __launch_bounds__(64 * kSegGroups) k3_reduce(Params p) {
   if (sg == 0 && active) {
     float4 t = s_num[0][h][d4];
     float dd = s_den[0][h];
-#pragma unroll
-    for (int g = 1; g < kSegGroups; ++g) {
+    for (int g = 1; g < groups; ++g) {
       const float4 u = s_num[g][h][d4];
       t.x += u.x;
       t.y += u.y;
@@ -92,20 +94,12 @@ __global__ void __launch_bounds__(64 * kSegGroups) k3_reduce(Params p) {
 
 cudaError_t launch_reduce(const Params& p, cudaStream_t stream) {
   dim3 grid(p.B, p.Hkv * p.HG, p.D / 32);
-  const bool many = p.max_seq_len_hint > 16384;  // long contexts split into many segments
-  if (p.D == 64) {
-    if (many)
-      k3_reduce<64, 4><<<grid, 256, 0, stream>>>(p);
-    else
-      k3_reduce<64, 1><<<grid, 64, 0, stream>>>(p);
-  } else if (p.D == 128) {
-    if (many)
-      k3_reduce<128, 4><<<grid, 256, 0, stream>>>(p);
-    else
-      k3_reduce<128, 1><<<grid, 64, 0, stream>>>(p);
-  } else {
+  if (p.D == 64)
+    k3_reduce<64><<<grid, 64 * kMaxGroups, 0, stream>>>(p);
+  else if (p.D == 128)
+    k3_reduce<128><<<grid, 64 * kMaxGroups, 0, stream>>>(p);
+  else
     return cudaErrorInvalidValue;
-  }
   return cudaGetLastError();
 }
 

@@ -145,7 +145,7 @@ template <typename T, int D, int RPW>
 cudaError_t launch_t(const Params& p, int grid, cudaStream_t stream) {
   size_t smem = generic_smem_bytes(p);
   auto kern = k4_generic<T, D, RPW>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
   if (e != cudaSuccess) return e;
   kern<<<grid, kWarps * 32, smem, stream>>>(p);
   return cudaGetLastError();

@@ -84,12 +84,13 @@ __global__ void __launch_bounds__(kMaxThreads) k5_metadata(Params p) {
   // pass 1: decode count and total decode KV blocks (+ the partition cost model's inputs:
   // K1 (Q block, 128-key tile) pairs and decode keys)
   int q0 = 0, L0 = 0;  // this thread's sequence when one_pass
-  unsigned long long my_blocks = 0, my_tiles = 0, my_keys = 0, my_dec = 0;
+  unsigned long long my_blocks = 0, my_tiles = 0, my_keys = 0, my_dec = 0, my_viol = 0;
   for (int b = threadIdx.x; b < B; b += nt) {
     const int qb = __ldg(p.cu_seqlens_q + b + 1) - __ldg(p.cu_seqlens_q + b);
     const int L = __ldg(p.seq_lens + b);
     q0 = qb;
     L0 = L;
+    my_viol += qb > p.max_query_len_hint ? 1ull : 0ull;  // the host planned with a smaller bound
     if (p.decode_to_k2 && qb == 1) {
       my_dec += 1;
       my_blocks += (unsigned long long)((L + p.bs - 1) / p.bs);
@@ -101,6 +102,7 @@ __global__ void __launch_bounds__(kMaxThreads) k5_metadata(Params p) {
     }
   }
   const unsigned long long n_dec = block_sum_u64(my_dec, s_red);
+  const unsigned long long n_viol = block_sum_u64(my_viol, s_red);
   const unsigned long long dec_blocks = block_sum_u64(my_blocks, s_red);
   unsigned long long tiles = 0, keys = 0;
   if (p.partition) {
@@ -145,10 +147,6 @@ __global__ void __launch_bounds__(kMaxThreads) k5_metadata(Params p) {
     carry_qb += tot.x;
     carry_ch += tot.y;
   }
-  if (p.fuse_reduce) {  // per-unit segment counters of K2's fused merge
-    const int n = B * p.Hkv * p.HG;
-    for (int i = threadIdx.x; i < n; i += nt) p.seg_cnt[i] = 0;
-  }
   if (threadIdx.x == 0) {
     p.cu_qb[B] = carry_qb;
     p.cu_ch[B] = carry_ch;
@@ -159,6 +157,7 @@ __global__ void __launch_bounds__(kMaxThreads) k5_metadata(Params p) {
     p.hdr[kHdrChunkBlocks] = (int)(C > INT_MAX ? INT_MAX : C);
     p.hdr[kHdrPrefillCounter] = 0;
     p.hdr[kHdrDecodeCounter] = 0;
+    p.hdr[kHdrHintViolation] = n_viol ? 1 : 0;
     // SM partition for concurrent K1 / K2: P minimising max(prefill time on P SMs, decode
     // time on the other SMs, capped by HBM), from per-SM rates of the two kernels.
     int P = p.num_sms;

@@ -7,6 +7,10 @@
 
 namespace pattn {
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device, size) instead of
+// on every launch (pattn_api.cu).
+cudaError_t ensure_dynamic_smem(const void* func, size_t bytes);
+
 // K5: batch metadata + decode segment plan (one CTA).
 cudaError_t launch_metadata(const Params& p, cudaStream_t stream);
 

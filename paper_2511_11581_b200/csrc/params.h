@@ -16,6 +16,7 @@ enum HdrWord {
   kHdrPrefillCounter = 5,  // dynamic work counters (reset by K5)
   kHdrDecodeCounter = 6,
   kHdrPrefillCtas = 7,   // two-stream SM partition: K1 CTAs that work (the rest exit at once)
+  kHdrHintViolation = 8, // K5: 1 if some q_b exceeds the max_query_len hint (the plan may miss it)
   kHdrWords = 64
 };
 
@@ -63,9 +64,8 @@ struct Params {
   float* part_m;      // [max_chunks][Hq]   (log2 domain: max of scale*log2e*s)
   float* part_l;      // [max_chunks][Hq]
   float* part_acc;    // [max_chunks][Hq][D]
-  int32_t* seg_cnt;   // [B][Hkv*HG] segments finished per decode unit (fused merge; zeroed by K5)
-  int32_t fuse_reduce;
-  int32_t max_seq_len_hint;  // host hint (max_seq_len, else max_blocks_per_seq * block_size)  // 1: the CTA finishing a unit's last segment merges the partials (no K3)
+  int32_t max_seq_len_hint;    // host hint (max_seq_len, else max_blocks_per_seq * block_size)
+  int32_t max_query_len_hint;  // host hint (max_query_len, else num_tokens); K5 flags q_b above it
 };
 
 }  // namespace pattn

@@ -9,7 +9,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <utility>
 #include <vector>
 
 #include "kernels.h"
@@ -59,6 +61,14 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
+bool debug_sync() {
+  static const bool on = [] {
+    const char* v = getenv("PATTN_DEBUG_SYNC");
+    return v && *v && *v != '0';
+  }();
+  return on;
+}
+
 int env_int(const char* name, int dflt) {
   const char* v = getenv(name);
   return (v && *v) ? atoi(v) : dflt;
@@ -75,6 +85,27 @@ pattn_status_t cuda_fail(cudaError_t e) {
   snprintf(g_last_error, sizeof(g_last_error), "%s: %s", cudaGetErrorName(e), cudaGetErrorString(e));
   return PATTN_ERR_CUDA;
 }
+
+}  // namespace
+
+namespace pattn {
+// Dynamic shared-memory opt-in, once per (kernel, device) and size (kernels.h).
+cudaError_t ensure_dynamic_smem(const void* func, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> g(mu);
+  size_t& have = done[{func, dev}];
+  if (have >= bytes) return cudaSuccess;
+  e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) have = bytes;
+  return e;
+}
+}  // namespace pattn
+
+namespace {
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 bool aligned16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15u) == 0; }
@@ -137,8 +168,7 @@ struct Plan {
   int target_items = 0, min_chunk = 1, split_mode = 0, max_chunks = 0;
   int num_sms = 148;
   size_t max_smem = 0;
-  size_t off_hdr = 0, off_cuqb = 0, off_cuch = 0, off_pm = 0, off_pl = 0, off_pacc = 0, off_cnt = 0, total = 0;
-  bool fuse_reduce = false;
+  size_t off_hdr = 0, off_cuqb = 0, off_cuch = 0, off_pm = 0, off_pl = 0, off_pacc = 0, total = 0;
   int k4_grid = 1;
   DecodeLaunch dl{};
   PrefillLaunch pl{};
@@ -190,6 +220,7 @@ void fill_params(const pattn_problem_t* p, const Plan& pl, Params* k) {
   k->kv_st_head = p->kv_stride_head;
   k->bt_stride = p->bt_stride;
   k->max_seq_len_hint = p->max_seq_len > 0 ? p->max_seq_len : p->max_blocks_per_seq * p->block_size;
+  k->max_query_len_hint = p->max_query_len > 0 ? p->max_query_len : p->num_tokens;
   k->o_st_tok = p->o_stride_tok;
   k->o_st_head = p->o_stride_head;
 }
@@ -271,12 +302,6 @@ pattn_status_t make_plan(const pattn_problem_t* p, const void* q, const void* kc
   off = align256(off + rows * sizeof(float));
   pl->off_pacc = off;
   off = align256(off + rows * (size_t)D * sizeof(float));
-  // decode segment merge: the separate K3 launch (default) or fused into K2's last CTA per unit
-  // (PATTN_K3_FUSED=1; measured slower: the per-item release fences and the serial merge by
-  // one CTA cost more than K3's launch -- config 2 +14 us, config 4 +117 us)
-  pl->fuse_reduce = pl->use_k2 && getenv("PATTN_K3_FUSED") != nullptr;
-  pl->off_cnt = off;
-  if (pl->fuse_reduce) off = align256(off + (size_t)p->num_seqs * p->num_kv_heads * pl->HG * sizeof(int32_t));
   pl->total = off;
 
   // grids
@@ -404,10 +429,42 @@ bool encode_o_map(CUtensorMap* tm, const pattn_problem_t* p, void* out) {
 
 struct EventRec {
   const pattn_exec_opts_t* o;
-  void rec(int idx, cudaStream_t s) const {
-    if (o && o->events[idx]) cudaEventRecord(static_cast<cudaEvent_t>(o->events[idx]), s);
+  cudaError_t rec(int idx, cudaStream_t s) const {
+    if (o && o->events[idx]) return cudaEventRecord(static_cast<cudaEvent_t>(o->events[idx]), s);
+    return cudaSuccess;
   }
 };
+
+// Fork/join events of the two-stream path, created once per (thread, device) and reused by
+// every call of that thread (recording an event again is legal, also during graph capture).
+struct ForkJoin {
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+cudaError_t fork_join_events(ForkJoin* out) {
+  static thread_local std::map<int, ForkJoin> cache;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  ForkJoin& fj = cache[dev];
+  if (!fj.fork && (e = cudaEventCreateWithFlags(&fj.fork, cudaEventDisableTiming)) != cudaSuccess) return e;
+  if (!fj.join && (e = cudaEventCreateWithFlags(&fj.join, cudaEventDisableTiming)) != cudaSuccess) return e;
+  *out = fj;
+  return cudaSuccess;
+}
+
+// Host-detectable argument errors of a call (before anything is enqueued).
+pattn_status_t check_call(const pattn_problem_t* p, const Plan& pl, const void* q, const void* k_cache,
+                          const void* v_cache, const int32_t* block_table, const int32_t* cu_seqlens_q,
+                          const int32_t* seq_lens, float scale, const void* out, const void* workspace,
+                          size_t workspace_bytes) {
+  (void)p;
+  if (!q || !k_cache || !v_cache || !block_table || !cu_seqlens_q || !seq_lens || !out || !workspace)
+    return PATTN_ERR_INVALID_ARG;
+  if ((reinterpret_cast<uintptr_t>(workspace) & 255u) != 0) return PATTN_ERR_INVALID_ARG;
+  if (workspace_bytes < pl.total) return PATTN_ERR_WORKSPACE_TOO_SMALL;
+  if (!(scale == scale) || scale > 3.0e38f || scale < -3.0e38f) return PATTN_ERR_INVALID_ARG;
+  return PATTN_OK;
+}
 
 pattn_status_t run(const pattn_problem_t* p, const void* q, const void* k_cache, const void* v_cache,
                    const int32_t* block_table, const int32_t* cu_seqlens_q, const int32_t* seq_lens, float scale,
@@ -416,11 +473,9 @@ pattn_status_t run(const pattn_problem_t* p, const void* q, const void* k_cache,
   Plan pl;
   pattn_status_t st = make_plan(p, q, k_cache, v_cache, out, &pl);
   if (st != PATTN_OK) return st;
-  if (!q || !k_cache || !v_cache || !block_table || !cu_seqlens_q || !seq_lens || !out || !workspace)
-    return PATTN_ERR_INVALID_ARG;
-  if ((reinterpret_cast<uintptr_t>(workspace) & 255u) != 0) return PATTN_ERR_INVALID_ARG;
-  if (workspace_bytes < pl.total) return PATTN_ERR_WORKSPACE_TOO_SMALL;
-  if (!(scale == scale) || scale > 3.0e38f || scale < -3.0e38f) return PATTN_ERR_INVALID_ARG;
+  st = check_call(p, pl, q, k_cache, v_cache, block_table, cu_seqlens_q, seq_lens, scale, out, workspace,
+                  workspace_bytes);
+  if (st != PATTN_OK) return st;
 
   cudaStream_t s1 = static_cast<cudaStream_t>(stream_v);
   cudaStream_t s2 = (opts && opts->stream2 && !(p->flags & PATTN_FLAG_SERIAL)) ? static_cast<cudaStream_t>(opts->stream2)
@@ -443,8 +498,6 @@ pattn_status_t run(const pattn_problem_t* p, const void* q, const void* k_cache,
   k.part_m = reinterpret_cast<float*>(ws + pl.off_pm);
   k.part_l = reinterpret_cast<float*>(ws + pl.off_pl);
   k.part_acc = reinterpret_cast<float*>(ws + pl.off_pacc);
-  k.seg_cnt = reinterpret_cast<int32_t*>(ws + pl.off_cnt);
-  k.fuse_reduce = pl.fuse_reduce ? 1 : 0;
 
   CUtensorMap tmQ, tmO, tmK5, tmV5;
   memset(&tmO, 0, sizeof(tmO));
@@ -474,60 +527,58 @@ pattn_status_t run(const pattn_problem_t* p, const void* q, const void* k_cache,
   }
 
   EventRec ev{opts};
-  cudaError_t e;
-  ev.rec(2 * PATTN_KERNEL_METADATA, s1);
-  e = launch_metadata(k, s1);
-  ev.rec(2 * PATTN_KERNEL_METADATA + 1, s1);
+  ForkJoin fj;
+  if (two) {
+    const cudaError_t e = fork_join_events(&fj);
+    if (e != cudaSuccess) return cuda_fail(e);
+  }
+  cudaError_t e = ev.rec(2 * PATTN_KERNEL_METADATA, s1);
+  if (e == cudaSuccess) e = launch_metadata(k, s1);
+  if (e == cudaSuccess) e = ev.rec(2 * PATTN_KERNEL_METADATA + 1, s1);
   if (e != cudaSuccess) return cuda_fail(e);
   if (metadata_only) return PATTN_OK;
 
-  cudaEvent_t fork = nullptr, join = nullptr;
   if (two) {
-    cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&join, cudaEventDisableTiming);
-    cudaEventRecord(fork, s1);
-    cudaStreamWaitEvent(s2, fork, 0);
+    e = cudaEventRecord(fj.fork, s1);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s2, fj.fork, 0);
+    if (e != cudaSuccess) return cuda_fail(e);
   }
   cudaStream_t sd = two ? s2 : s1;
   // Two streams: the prefill kernel is issued first so that its (one-per-SM) CTAs take
   // their SMs before the decode grid spreads over the GPU; the CTAs beyond K5's partition
   // exit at once, the decode CTAs fill those SMs and, claiming items dynamically, the SMs
-  // the prefill CTAs release when they finish.
-  if (pl.use_k1) {
-    ev.rec(2 * PATTN_KERNEL_PREFILL, s1);
-    e = launch_prefill(k, pl.pl, tmQ, tmO, head_maps, s1);
-    ev.rec(2 * PATTN_KERNEL_PREFILL + 1, s1);
-    if (e != cudaSuccess) return cuda_fail(e);
-  }
+  // the prefill CTAs release when they finish.  After the fork, every exit path records the
+  // join so that stream2 is always joined back (a capture stays well formed).
+  auto step = [&](int kind, cudaStream_t s, auto&& launch) {
+    if (e != cudaSuccess) return;
+    e = ev.rec(2 * kind, s);
+    if (e == cudaSuccess) e = launch();
+    if (e == cudaSuccess) e = ev.rec(2 * kind + 1, s);
+  };
+  if (pl.use_k1) step(PATTN_KERNEL_PREFILL, s1, [&] { return launch_prefill(k, pl.pl, tmQ, tmO, head_maps, s1); });
   if (pl.use_k2) {
-    ev.rec(2 * PATTN_KERNEL_DECODE, sd);
-    e = launch_decode(k, pl.dl, tmK5, tmV5, sd);
-    ev.rec(2 * PATTN_KERNEL_DECODE + 1, sd);
-    if (e != cudaSuccess) return cuda_fail(e);
-    if (!pl.fuse_reduce) {
-      ev.rec(2 * PATTN_KERNEL_REDUCE, sd);
-      e = launch_reduce(k, sd);
-      ev.rec(2 * PATTN_KERNEL_REDUCE + 1, sd);
-      if (e != cudaSuccess) return cuda_fail(e);
-    }
+    step(PATTN_KERNEL_DECODE, sd, [&] { return launch_decode(k, pl.dl, tmK5, tmV5, sd); });
+    step(PATTN_KERNEL_REDUCE, sd, [&] { return launch_reduce(k, sd); });
   }
-  if (pl.use_k7) {
-    ev.rec(2 * PATTN_KERNEL_BASELINE, s1);
-    e = launch_baseline(k, s1);
-    ev.rec(2 * PATTN_KERNEL_BASELINE + 1, s1);
-    if (e != cudaSuccess) return cuda_fail(e);
-  }
-  if (pl.use_k4) {
-    ev.rec(2 * PATTN_KERNEL_GENERIC, s1);
-    e = launch_generic(k, pl.k4_grid, pl.rpw, s1);
-    ev.rec(2 * PATTN_KERNEL_GENERIC + 1, s1);
-    if (e != cudaSuccess) return cuda_fail(e);
-  }
+  if (pl.use_k7) step(PATTN_KERNEL_BASELINE, s1, [&] { return launch_baseline(k, s1); });
+  if (pl.use_k4) step(PATTN_KERNEL_GENERIC, s1, [&] { return launch_generic(k, pl.k4_grid, pl.rpw, s1); });
   if (two) {
-    cudaEventRecord(join, s2);
-    cudaStreamWaitEvent(s1, join, 0);
-    cudaEventDestroy(fork);
-    cudaEventDestroy(join);
+    cudaError_t ej = cudaEventRecord(fj.join, s2);
+    if (ej == cudaSuccess) ej = cudaStreamWaitEvent(s1, fj.join, 0);
+    if (e == cudaSuccess) e = ej;
+  }
+  if (e != cudaSuccess) return cuda_fail(e);
+  if (debug_sync()) {
+    // PATTN_DEBUG_SYNC=1: synchronise and check what the device saw against the host hints
+    // (a max_query_len hint below the true maximum can drop the prefill kernel from the plan)
+    int32_t viol = 0;
+    e = cudaStreamSynchronize(s1);
+    if (e == cudaSuccess) e = cudaMemcpy(&viol, k.hdr + kHdrHintViolation, sizeof(viol), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(e);
+    if (viol) {
+      snprintf(g_last_error, sizeof(g_last_error), "a sequence's q_b exceeds the max_query_len hint");
+      return PATTN_ERR_INVALID_SEQUENCE;
+    }
   }
   return PATTN_OK;
 }
@@ -605,6 +656,17 @@ pattn_status_t pattn_unified_attention_hostio(const pattn_problem_t* p, const vo
   HostIoLayout L;
   if (!hostio_layout(p, &L)) return PATTN_ERR_INVALID_ARG;
   if (workspace_bytes < L.total) return PATTN_ERR_WORKSPACE_TOO_SMALL;
+  {
+    // everything run() checks on the host, checked before the copies are enqueued
+    Plan pl;
+    uint8_t* w8 = static_cast<uint8_t*>(workspace);
+    st = make_plan(p, w8 + L.q, k_cache, v_cache, w8 + L.out, &pl);
+    if (st == PATTN_OK)
+      st = check_call(p, pl, w8 + L.q, k_cache, v_cache, reinterpret_cast<int32_t*>(w8 + L.bt),
+                      reinterpret_cast<int32_t*>(w8 + L.cu), reinterpret_cast<int32_t*>(w8 + L.sl), scale, w8 + L.out,
+                      workspace, L.base);
+    if (st != PATTN_OK) return st;
+  }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   uint8_t* ws = static_cast<uint8_t*>(workspace);
   const size_t esz = p->dtype == PATTN_DTYPE_F32 ? 4 : 2;
@@ -684,14 +746,14 @@ int32_t pattn_planned_launches(const pattn_problem_t* p) {
   Plan pl;
   if (make_plan(p, nullptr, nullptr, nullptr, nullptr, &pl) != PATTN_OK) return 0;
   return 1 + (pl.use_k1 ? 1 : 0) + (pl.use_k4 ? 1 : 0) + (pl.use_k7 ? 1 : 0) +
-         (pl.use_k2 ? (pl.fuse_reduce ? 1 : 2) : 0);
+         (pl.use_k2 ? 2 : 0);
 }
 
 int32_t pattn_planned_kernels(const pattn_problem_t* p) {
   Plan pl;
   if (make_plan(p, nullptr, nullptr, nullptr, nullptr, &pl) != PATTN_OK) return 0;
   return (1 << PATTN_KERNEL_METADATA) | (pl.use_k1 ? 1 << PATTN_KERNEL_PREFILL : 0) |
-         (pl.use_k2 ? (1 << PATTN_KERNEL_DECODE) | (pl.fuse_reduce ? 0 : 1 << PATTN_KERNEL_REDUCE) : 0) |
+         (pl.use_k2 ? (1 << PATTN_KERNEL_DECODE) | (1 << PATTN_KERNEL_REDUCE) : 0) |
          (pl.use_k4 ? 1 << PATTN_KERNEL_GENERIC : 0) | (pl.use_k7 ? 1 << PATTN_KERNEL_BASELINE : 0);
 }
 

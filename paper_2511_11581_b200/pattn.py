@@ -213,21 +213,67 @@ def make_problem(
 
 
 class _Workspace:
-    """Per-device cached workspace (grows, never shrinks)."""
+    """Cached default workspaces, one per (device, stream): two calls on different streams
+    never share one (the C ABI requires distinct workspaces for concurrent calls).  A buffer
+    that is outgrown is retired but kept alive (never returned to the caching allocator), so
+    kernels still in flight on any stream and CUDA graphs captured with it stay valid."""
 
     def __init__(self):
         self.buf = {}
+        self.retired = []
+        self.lock = threading.Lock()
 
-    def get(self, nbytes: int, device: torch.device) -> torch.Tensor:
-        key = device.index if device.index is not None else torch.cuda.current_device()
-        b = self.buf.get(key)
-        if b is None or b.numel() < nbytes:
-            b = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
-            self.buf[key] = b
-        return b
+    def get(self, nbytes: int, device: torch.device, stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+        dev = device.index if device.index is not None else torch.cuda.current_device()
+        s = stream if stream is not None else torch.cuda.current_stream(dev)
+        key = (dev, int(s.cuda_stream))
+        with self.lock:
+            b = self.buf.get(key)
+            if b is None or b.numel() < nbytes:
+                if b is not None:
+                    self.retired.append(b)
+                b = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=torch.device("cuda", dev))
+                self.buf[key] = b
+            return b
 
 
 _ws = _Workspace()
+
+
+def _validate(q, k_cache, v_cache, block_table, cu_seqlens_q, seq_lens, out, kv_layout, host_io=False):
+    """Host-side argument checks the C ABI cannot make from raw pointers: V has
+    K's shape/strides/dtype (the library reads V with K's strides), out matches q, the caches
+    match q's dtype, metadata is int32 with unit inner stride, and everything lives where the
+    call expects it.  Raises PattnError(PATTN_ERR_INVALID_ARG) on any mismatch."""
+    if v_cache.shape != k_cache.shape or v_cache.stride() != k_cache.stride():
+        raise PattnError(1, "v_cache must have k_cache's shape and strides")
+    if k_cache.dtype != q.dtype or v_cache.dtype != q.dtype:
+        raise PattnError(1, f"cache dtype {k_cache.dtype}/{v_cache.dtype} != q dtype {q.dtype}")
+    if out.shape != q.shape or out.dtype != q.dtype:
+        raise PattnError(1, f"out {tuple(out.shape)}/{out.dtype} must match q {tuple(q.shape)}/{q.dtype}")
+    if q.dim() != 3 or k_cache.dim() != 4 or block_table.dim() != 2:
+        raise PattnError(1, "q must be [T, Hq, D], caches 4-D, block_table 2-D")
+    for name, t in (("block_table", block_table), ("cu_seqlens_q", cu_seqlens_q), ("seq_lens", seq_lens)):
+        if t.dtype != torch.int32:
+            raise PattnError(1, f"{name} must be int32 (got {t.dtype})")
+        if t.stride(-1) != 1:
+            raise PattnError(1, f"{name} must have unit inner stride")
+    B = seq_lens.shape[0]
+    if cu_seqlens_q.dim() != 1 or cu_seqlens_q.shape[0] != B + 1 or block_table.shape[0] < B:
+        raise PattnError(1, "cu_seqlens_q must have num_seqs + 1 entries and block_table num_seqs rows")
+    if not (k_cache.is_cuda and v_cache.is_cuda):
+        raise PattnError(1, "k_cache / v_cache must be CUDA tensors")
+    dev = k_cache.device
+    if v_cache.device != dev:
+        raise PattnError(1, "k_cache and v_cache on different devices")
+    rest = (q, out, block_table, cu_seqlens_q, seq_lens)
+    if host_io:
+        if any(t.is_cuda for t in rest):
+            raise PattnError(1, "hostio: q, out and the metadata must be host tensors")
+        if not all(t.is_contiguous() for t in rest):
+            raise PattnError(1, "hostio: q, out and the metadata must be contiguous")
+    elif any(t.device != dev for t in rest):
+        raise PattnError(1, "all tensors must be on the caches' CUDA device")
 
 
 def workspace_size(problem: Problem) -> int:
@@ -268,12 +314,18 @@ def unified_attention(
     lib = load()
     if out is None:
         out = torch.empty_like(q)
+    _validate(q, k_cache, v_cache, block_table, cu_seqlens_q, seq_lens, out, kv_layout)
     B = seq_lens.shape[0]
     p = make_problem(q, k_cache, num_kv_heads, block_size, block_table, B, out, kv_layout, max_query_len,
                      max_seq_len, flags)
     need = workspace_size(p)
-    ws = workspace if workspace is not None else _ws.get(need, q.device)
     s = stream if stream is not None else torch.cuda.current_stream(q.device)
+    if workspace is None:
+        ws = _ws.get(need, q.device, s)  # per (device, stream); never freed while a graph may use it
+    else:
+        ws = workspace
+        if ws.numel() < need:
+            raise PattnError(6, f"workspace of {ws.numel()} bytes < {need}")
     args = (
         ctypes.byref(p), q.data_ptr(), k_cache.data_ptr(), v_cache.data_ptr(), block_table.data_ptr(),
         cu_seqlens_q.data_ptr(), seq_lens.data_ptr(), ctypes.c_float(scale), out.data_ptr(), ws.data_ptr(),
@@ -313,14 +365,16 @@ def unified_attention_hostio(
     """End-to-end call: q / metadata / out are (pinned) HOST tensors, the caches are on the device.
     The H2D copies, the attention and the D2H copy are enqueued on `stream`; sync before reading out_host."""
     lib = load()
+    _validate(q_host, k_cache, v_cache, block_table_host, cu_seqlens_q_host, seq_lens_host, out_host, kv_layout,
+              host_io=True)
     B = seq_lens_host.shape[0]
     p = make_problem(q_host, k_cache, num_kv_heads, block_size, block_table_host, B, out_host, kv_layout,
                      max_query_len, max_seq_len, flags)
     need = int(lib.pattn_hostio_workspace_size(ctypes.byref(p)))
     if need == 0:
         raise PattnError(1, "pattn_hostio_workspace_size")
-    ws = workspace if workspace is not None else _ws.get(need, k_cache.device)
     s = stream if stream is not None else torch.cuda.current_stream(k_cache.device)
+    ws = workspace if workspace is not None else _ws.get(need, k_cache.device, s)
     _check(
         lib.pattn_unified_attention_hostio(
             ctypes.byref(p), q_host.data_ptr(), k_cache.data_ptr(), v_cache.data_ptr(), block_table_host.data_ptr(),
@@ -380,8 +434,8 @@ def debug_plan(problem: Problem, cu_seqlens_q: torch.Tensor, seq_lens: torch.Ten
     cap = 2 * B + 10
     plan = torch.full((cap,), -7, dtype=torch.int32, device=cu_seqlens_q.device)
     need = workspace_size(problem)
-    ws = _ws.get(need, cu_seqlens_q.device)
     s = torch.cuda.current_stream(cu_seqlens_q.device)
+    ws = _ws.get(need, cu_seqlens_q.device, s)
     _check(
         lib.pattn_debug_plan(ctypes.byref(problem), cu_seqlens_q.data_ptr(), seq_lens.data_ptr(), plan.data_ptr(), cap,
                              ws.data_ptr(), ws.numel(), s.cuda_stream),
@@ -424,15 +478,11 @@ def make_events(n_steps: int):
     return out
 
 
-def last_prefill_sms(device=None) -> int:
-    """K1's SM count chosen by K5 in the last call that used the cached workspace (header word
+def workspace_prefill_sms(workspace: torch.Tensor) -> int:
+    """K1's SM count chosen by K5 in the last call that used `workspace` (header word
     kHdrPrefillCtas): the two-stream partition, or all SMs when serial.  Reads 4
     bytes device->host (synchronous); for reporting only, never on the hot path."""
-    dev = torch.device("cuda", device if device is not None else torch.cuda.current_device())
-    b = _ws.buf.get(dev.index)
-    if b is None:
-        raise RuntimeError("no cached workspace on this device")
-    return int(b[28:32].view(torch.int32).item())
+    return int(workspace[28:32].view(torch.int32).item())
 
 
 def version() -> int:

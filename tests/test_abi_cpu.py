@@ -86,10 +86,8 @@ def test_workspace_and_planned_launches(lib, monkeypatch):
     pb = _problem(lib, Hq=32, Hkv=8, D=128, dtype=1, T=64, B=64, nb=16448, maxb=257)
     pb.max_query_len = 1
     assert lib.planned_launches(pb) == 3  # metadata + decode + reduce
-    monkeypatch.setenv("PATTN_K3_FUSED", "1")
-    assert lib.planned_launches(pb) == 2  # metadata + decode (segment merge fused into K2)
-    assert lib.planned_kernels(pb) == (1 << lib.KERNEL_METADATA) | (1 << lib.KERNEL_DECODE)
-    monkeypatch.delenv("PATTN_K3_FUSED")
+    assert lib.planned_kernels(pb) == (1 << lib.KERNEL_METADATA) | (1 << lib.KERNEL_DECODE) | (
+        1 << lib.KERNEL_REDUCE)
     pb.max_query_len = 2048
     assert lib.planned_launches(pb) == 4  # + the Q-block kernel
     pb.flags = lib.FLAG_FORCE_GENERIC

@@ -1,6 +1,8 @@
 """GPU parity: libpattn (through its C ABI) vs the fp64 oracle, element by element, on the
 same seeded inputs (workloads/).  Tolerances from north_star: bf16 |err| <= 1e-2 + 1e-2|ref|,
 fp32 |err| <= 1e-5 + 1e-5|ref|; indexing bit-exact (needle tests, debug_plan)."""
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -346,22 +348,92 @@ def test_strided_out_and_q_canary():
 
 
 @pytest.mark.parametrize("flags", [0, 0x4])
-def test_fused_segment_merge_equals_separate_reduce(flags, monkeypatch):
-    """The decode segment merge fused into K2 (last CTA of a unit merges, PATTN_K3_FUSED=1) and
-    the separate K3 launch (default) both match the oracle; many segments per unit."""
-    w = Workload("fuse", ((20000, 1), (0, 40), (3000, 1), (17, 1), (9000, 1)), 64, 8, 128, 16, "bf16")
+def test_segment_reduce_groups_follow_segment_count(flags):
+    """K3 picks its segment-group count from each sequence's actual number of segments (1 group
+    for a few, up to 4 for many): sequences from 1 to several hundred segments in one batch,
+    against the oracle, and bitwise reproducible."""
+    w = Workload("k3groups", ((20000, 1), (0, 40), (3000, 1), (17, 1), (9000, 1), (60000, 1)), 64, 8, 128, 16,
+                 "bf16")
     batch = generate(w, seed=13, dist="peaked")
     ref = O.batch_attention(batch)
     db = DeviceBatch(batch)
-    sep = db.run(flags=flags).clone()
-    monkeypatch.setenv("PATTN_K3_FUSED", "1")
-    assert P.planned_kernels(P.make_problem(db.q, db.k, 8, 16, db.bt, 5)) & (1 << P.KERNEL_REDUCE) == 0
-    fused = db.run(flags=flags).clone()
-    assert_close(out_f64(fused), ref, "bf16", "fused merge")
-    assert_close(out_f64(sep), ref, "bf16", "separate K3")
-    again = db.run(flags=flags)
-    assert torch.equal(again, fused)  # deterministic whichever CTA finishes a unit last
-    monkeypatch.delenv("PATTN_K3_FUSED")
+    a = db.run(flags=flags).clone()
+    assert_close(out_f64(a), ref, "bf16", f"K3 groups flags={flags}")
+    assert torch.equal(db.run(flags=flags), a)
+
+
+def test_hintless_call_matches_oracle():
+    """No host hints (max_query_len / max_seq_len = 0): the planner uses its upper bounds."""
+    w = Workload("nohint", ((0, 300), (2500, 1), (64, 40), (900, 1)), 32, 8, 128, 16, "bf16")
+    batch = generate(w, seed=21, dist="peaked", poison=True)
+    db = DeviceBatch(batch)
+    o = P.unified_attention(db.q, db.k, db.v, db.bt, db.cu, db.sl, w.scale, w.num_kv_heads, w.block_size)
+    torch.cuda.synchronize()
+    assert_close(out_f64(o), O.batch_attention(batch), "bf16", "hint-less")
+
+
+def test_hint_violation_detected_in_debug_mode(monkeypatch):
+    """A max_query_len hint below the true maximum drops the Q-block kernel from the plan; with
+    PATTN_DEBUG_SYNC=1 the call synchronises and reports it (PATTN_ERR_INVALID_SEQUENCE)."""
+    import subprocess
+    import sys
+
+    code = r"""
+import os, sys, torch
+sys.path.insert(0, os.getcwd())
+from paper_2511_11581_b200 import pattn as P
+from workloads import Workload, generate
+from gpu_helpers import DeviceBatch
+w = Workload("viol", ((0, 50), (700, 1)), 32, 8, 128, 16, "bf16")
+db = DeviceBatch(generate(w, seed=3))
+try:
+    P.unified_attention(db.q, db.k, db.v, db.bt, db.cu, db.sl, w.scale, 8, 16, max_query_len=1, max_seq_len=701)
+    print("no error")
+except P.PattnError as e:
+    print("code", e.code)
+"""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PATTN_DEBUG_SYNC="1", PYTHONPATH=os.path.join(root, "tests"))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=300)
+    assert "code 3" in r.stdout, r.stdout + r.stderr[-2000:]
+
+
+def test_binding_rejects_mismatched_tensors():
+    """the binding checks what raw pointers cannot carry (V vs K strides, out vs q,
+    int32 metadata, one device) and raises PATTN_ERR_INVALID_ARG before calling the library."""
+    w = Workload("val", ((0, 20), (100, 1)), 32, 8, 128, 16, "bf16")
+    db = DeviceBatch(generate(w, seed=4))
+    args = lambda **kw: dict(dict(q=db.q, k_cache=db.k, v_cache=db.v, block_table=db.bt, cu_seqlens_q=db.cu,
+                                  seq_lens=db.sl, scale=w.scale, num_kv_heads=8, block_size=16), **kw)
+    bad = [
+        dict(v_cache=db.v[:, :, :4]),
+        dict(out=torch.empty_like(db.q, dtype=torch.float32)),
+        dict(out=torch.empty((db.q.shape[0] + 1,) + tuple(db.q.shape[1:]), dtype=db.q.dtype, device="cuda")),
+        dict(cu_seqlens_q=db.cu.long()),
+        dict(seq_lens=db.sl.cpu()),
+        dict(k_cache=db.k.float(), v_cache=db.v.float()),
+    ]
+    for kw in bad:
+        with pytest.raises(P.PattnError) as ei:
+            P.unified_attention(**args(**kw))
+        assert ei.value.code == 1, kw.keys()
+
+
+def test_default_workspace_is_per_stream():
+    """Two calls on different streams without explicit workspaces get different cached buffers."""
+    w = Workload("ws", ((0, 64), (900, 1), (1200, 1)), 32, 8, 128, 16, "bf16")
+    batch = generate(w, seed=5, dist="peaked")
+    db = DeviceBatch(batch)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    o1, o2 = torch.empty_like(db.q), torch.empty_like(db.q)
+    for _ in range(3):
+        db.run(out=o1, stream=s1)
+        db.run(out=o2, stream=s2)
+    torch.cuda.synchronize()
+    keys = [k for k in P._ws.buf if k[1] in (s1.cuda_stream, s2.cuda_stream)]
+    assert len(keys) == 2
+    assert torch.equal(o1, o2)
+    assert_close(out_f64(o1), O.batch_attention(batch), "bf16", "per-stream workspace")
 
 
 @pytest.mark.parametrize("case", [0, 4, 5, 6, 7, 8])
