@@ -251,6 +251,30 @@ PATTN_API pattn_status_t pattn_set_tuning_tree(const pattn_tree_node_t* nodes, i
  * defaults resolved), written to *out.  No device work. */
 PATTN_API pattn_status_t pattn_plan_tuning(const pattn_problem_t* p, pattn_tuning_t* out);
 
+/*
+ * CUDA-graph capture of the unified call ("full graph" execution, §6.2 P:180-199:
+ * graphs are recorded per batch-size bucket at startup and replayed; the static launch grid
+ * of §4.7 P:401-406 makes one recording valid for every batch that fits the bucket).
+ *   pattn_graph_capture: records ONE pattn_unified_attention_ex call on `stream` (with
+ *     `stream2` as the concurrent decode branch when non-NULL) into an executable graph.
+ *     Every pointer passed is baked into the graph: they must stay valid, and the caller
+ *     refreshes the CONTENTS of q / block_table / cu_seqlens_q / seq_lens between launches
+ *     (the grids never depend on them; sequences with q_b = 0 pad a bucket).  Sizes in *p
+ *     (num_seqs, num_tokens, hints) are the bucket's capacities.  `stream` must not be
+ *     capturing already.  Returns PATTN_OK and a handle in *graph.
+ *   pattn_graph_launch: replays the graph on `stream` (asynchronous).
+ *   pattn_graph_destroy: frees the handle (host-side graph objects only; no device memory
+ *     is owned).  The graph must not be in flight.
+ */
+typedef struct pattn_graph* pattn_graph_t;
+PATTN_API pattn_status_t pattn_graph_capture(const pattn_problem_t* p, const void* q, const void* k_cache,
+                                             const void* v_cache, const int32_t* block_table,
+                                             const int32_t* cu_seqlens_q, const int32_t* seq_lens, float scale,
+                                             void* out, void* workspace, size_t workspace_bytes, void* stream,
+                                             void* stream2, pattn_graph_t* graph);
+PATTN_API pattn_status_t pattn_graph_launch(pattn_graph_t graph, void* stream);
+PATTN_API pattn_status_t pattn_graph_destroy(pattn_graph_t graph);
+
 /* Static string for a status code. */
 PATTN_API const char* pattn_status_string(pattn_status_t s);
 

@@ -102,6 +102,13 @@ PATTN_DEVICE void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
                "r"(bytes)
                : "memory");
 }
+// try_wait suspend-time hint.  Default: none (the instruction's own system-dependent window);
+// -DPATTN_MBAR_SLEEP_HINT restores a 10 ms hint (ptxas then emits NANOSLEEP.SYNCS on a miss).
+#ifdef PATTN_MBAR_SLEEP_HINT
+#define PATTN_MBAR_HINT ", 10000000"
+#else
+#define PATTN_MBAR_HINT ""
+#endif
 PATTN_DEVICE void mbar_wait_tag(uint64_t* bar, uint32_t parity, int t0, int t1, int t2) {
 #ifdef PATTN_WATCHDOG
   for (uint32_t n = 0;; ++n) {
@@ -127,7 +134,7 @@ PATTN_DEVICE void mbar_wait_tag(uint64_t* bar, uint32_t parity, int t0, int t1, 
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 10000000;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1" PATTN_MBAR_HINT ";\n\t"
       "@!p bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
@@ -156,10 +163,17 @@ PATTN_DEVICE void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 10000000;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1" PATTN_MBAR_HINT ";\n\t"
       "@!p bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+}
+
+// Physical SM of the calling thread (%smid) -- used by the two-stream SM partition.
+PATTN_DEVICE int sm_id() {
+  uint32_t id;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(id));
+  return (int)id;
 }
 
 // Non-blocking: has the phase with this parity completed?

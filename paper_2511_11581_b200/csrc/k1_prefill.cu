@@ -93,6 +93,7 @@ constexpr int kThreads = 512;  // 16 warps
 #define PATTN_K1_REG_WG3 40
 #endif
 constexpr int kRegWG0 = PATTN_K1_REG_WG0, kRegSoftmax = PATTN_K1_REG_SOFTMAX, kRegWG3 = PATTN_K1_REG_WG3;
+// setmaxnreg only redistributes the CTA's launch allocation
 static_assert(128 * (kRegWG0 + kRegWG3) + 256 * kRegSoftmax <= 65536, "register budget");
 constexpr uint32_t kQTile = kHalfM * kD * 2;  // 32 KB: one 128-row half of the Q block
 constexpr uint32_t kHalf = kQTile / 2;         // 16 KB: one 64-wide d half of it
@@ -108,12 +109,6 @@ constexpr uint32_t kSub16Bytes = 16 * kD * 2;  // 4 KB: one 16-key sub-block of 
 #endif
 constexpr int kKStages = PATTN_K1_KST;
 constexpr int kVStages = PATTN_K1_VST;  // V waits on PV (later than S), so it gets the deeper ring
-#ifndef PATTN_K1_TRUNC
-#define PATTN_K1_TRUNC 0
-#endif
-#ifndef PATTN_K1_PP
-#define PATTN_K1_PP 0
-#endif
 constexpr float kRescaleThreshold = 8.0f;  // log2 domain: rescale O only if the max grows by > 2^8
 
 // shared-memory map (offsets from a 1024-aligned base)
@@ -231,8 +226,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t sbase = smem_u32(smem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   PATTN_CTA_BEGIN(k1);
-  // two-stream SM partition (K5's choice): surplus CTAs leave their SM to the decode kernel
+  // two-stream SM partition (K5's choice): K1 works on the SMs with %smid < P; a CTA placed on
+  // another SM leaves it to the decode kernel at once.  Keyed on the physical SM (not blockIdx),
+  // so it holds whichever kernel the hardware (or a replayed CUDA graph, whose two branches
+  // start in either order) launches first.  CTA 0 always works (progress guarantee).
+#ifdef PATTN_PARTITION_BLOCKIDX  // A/B: the round-1 rule (CTA index, launch-order dependent)
   if (p.partition && (int)blockIdx.x >= p.hdr[kHdrPrefillCtas]) return;
+#else
+  if (p.partition && blockIdx.x != 0 && sm_id() >= p.hdr[kHdrPrefillCtas]) return;
+#endif
 #ifdef PATTN_TRACE
   const int trace_role = warp == 15 ? -1 : warp == 1 ? 0 : warp == 0 ? 3 : warp == 3 ? 4 : warp == 4 ? 1 : 2;
   unsigned int trace_cnt = 0;
@@ -472,7 +474,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (x.ntiles < 0) break;
         if (lane == 0) {
           mbar_wait(&bar.q_empty, (ic & 1u) ^ 1u);
-          mbar_arrive_expect_tx(&bar.q_full, 2 * kQTile);
+          mbar_arrive_expect_tx(&bar.q_full, 4u * (uint32_t)(bq_half * G) * 128u);  // 2 halves x 2 d-halves
           for (int h = 0; h < 2; ++h) {
             const int tok = x.q0 + x.tok0 + h * bq_half;
             tma_load_4d(smem + kOffQ + h * kQTile, &tmQ, &bar.q_full, 0, 0, x.kvh, tok);
@@ -490,6 +492,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t lane_off = (uint32_t)(32 * (warp & 3)) << 16;
     const uint32_t tS0 = tmem + kTmemS + 128 * h + lane_off;
     const uint32_t tO = tmem + kTmemO + 128 * h + lane_off;
+    const bool lead = r == 0;  // trace recorder
     uint32_t tc = 0, vc = 0;  // tiles seen by this warpgroup (== PV count of this half)
     uint32_t sc0 = 0u, sc1 = 0u;  // completed phases observed per S buffer (scalars: a runtime-indexed
                                   // array would live in local memory inside the tile loop)
@@ -497,13 +500,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float cs = p.scale_log2;
     const float ca = fmaxf(fabsf(cs), 1e-30f);  // scale 0: -inf * 0 would be NaN; 1e-30 * s ~ 0
     uint32_t ic = 0;
-    if (PATTN_K1_PP && h == 1) named_bar_arrive(1, 256);  // half a goes first
     for (;; ++ic) {
       const Item x = next_item(bar, ring, ic, lane);
       if (x.ntiles < 0) break;
       const int tk = h * bq_half + r / G;  // token of this row within the Q block
-      const bool row_valid = tk < x.ntok;
-      const int row_lim = min(x.ctx + x.tok0 + tk + 1, x.kv_end);  // keys [0, row_lim) visible
+      // G not dividing 128: rows r >= bq_half * G of a half are padding (their Q rows are never
+      // loaded); they see no key (fully masked, never stored)
+      const bool row_live = r < bq_half * G;
+      const bool row_valid = row_live && tk < x.ntok;
+      const int row_lim = row_live ? min(x.ctx + x.tok0 + tk + 1, x.kv_end) : 0;  // keys [0, row_lim) visible
       const int nsb_valid = (x.kv_end + 15) / 16;                  // 16-key sub-blocks fetched
       float m_run = -INFINITY, l_run = 0.f;
       float s[kN];
@@ -513,7 +518,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&bar.s_full[h][sb], (sb ? sc1 : sc0) & 1u);
         sc0 += sb ? 0u : 1u;
         sc1 += sb ? 1u : 0u;
-        if (r == 0) PATTN_K1_TRACE(10 + h);
+        if (lead) PATTN_K1_TRACE(10 + h);
         tc_fence_after();
         {
           uint32_t* su = reinterpret_cast<uint32_t*>(s);
@@ -521,7 +526,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           PATTN_TMEM_LD32(tS + 32, (su + 32));
           tmem_wait_ld();
         }
-        if (r == 0) PATTN_K1_TRACE(30 + h);
+        if (lead) PATTN_K1_TRACE(30 + h);
         const int key0 = jt * kN;
         const int nvis = row_lim - key0;  // keys [key0, key0 + nvis) of this tile are visible
         if (cs < 0.f) {  // sign-adjust so that max(raw) * |c| = max(scaled)
@@ -538,8 +543,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int c = 8; c < kN; ++c) mx[c & 7] = fmaxf(mx[c & 7], s[c]);
         const float mraw = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
-                                 fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
-        if (r == 0) PATTN_K1_TRACE(32 + h);
+                           fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+        if (lead) PATTN_K1_TRACE(32 + h);
         const float mt = mraw * ca;
         const float m_new = fmaxf(m_run, mt);
         float alpha = 1.f, m_use = m_run;
@@ -553,33 +558,26 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint64_t ca2 = f32x2(ca, ca), nb2 = f32x2(nbase, nbase);
         uint64_t rs2[4] = {0ull, 0ull, 0ull, 0ull};
         uint32_t pk[kN / 2];
-        if (PATTN_K1_PP) named_bar_sync(h ? 2 : 1, 256);
 #pragma unroll
         for (int c = 0; c < kN; c += 2) {
           // e^{scale*qk - m} in the log2 domain
           const uint64_t xx = ffma2(f32x2(s[c], s[c + 1]), ca2, nb2);
           const float e0 = fast_exp2(f32x2_lo(xx)), e1 = fast_exp2(f32x2_hi(xx));
           rs2[(c >> 1) & 3] = fadd2(rs2[(c >> 1) & 3], f32x2(e0, e1));
-#if PATTN_K1_TRUNC
-          pk[c >> 1] = __byte_perm(__float_as_uint(e0), __float_as_uint(e1), 0x7632);
-#else
           pk[c >> 1] = pack_bf16(e0, e1);
-#endif
         }
-        if (PATTN_K1_PP) named_bar_arrive(h ? 1 : 2, 256);
         const uint64_t r01 = fadd2(rs2[0], rs2[1]), r23 = fadd2(rs2[2], rs2[3]), rr = fadd2(r01, r23);
         const float rs = f32x2_lo(rr) + f32x2_hi(rr);
-        if (r == 0) PATTN_K1_TRACE(34 + h);
+        if (lead) PATTN_K1_TRACE(34 + h);
         // O_h: PV_h(jt-1) (issued once P_h(jt-1) arrived, while this tile's exponentials ran)
         // must be complete before O_h is corrected and before P_h(jt) can be consumed.
-        const bool need_rescale = __any_sync(0xffffffffu, alpha != 1.f);
         // (the wait cannot be skipped when no row rescales: mbarrier parity only tells phases
         // apart one step back, so every pv_done phase must be observed in order)
         if (jt > 0) {
           mbar_wait(&bar.pv_done[h], (tc - 1) & 1u);
           tc_fence_after();
           // tcgen05.ld/st are warp-collective (.sync.aligned): rescale when ANY row of the warp needs it
-          if (need_rescale) {
+          if (__any_sync(0xffffffffu, alpha != 1.f)) {
 #pragma unroll
             for (int c0 = 0; c0 < kD; c0 += 32) {
               uint32_t o[32];
@@ -614,24 +612,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         ++vc;
         tmem_wait_st();
         tc_fence_before();
-        if (r == 0) PATTN_K1_TRACE(12 + h);
+        if (lead) PATTN_K1_TRACE(12 + h);
         mbar_arrive(&bar.p_full[h]);
         ++tc;
       }
       // ---- epilogue: O / l -> bf16 -> out (valid rows only)
       mbar_wait(&bar.pv_done[h], (tc - 1) & 1u);
-      if (r == 0) PATTN_K1_TRACE(42 + h);
+      if (lead) PATTN_K1_TRACE(42 + h);
       tc_fence_after();
-      const float inv = 1.f / l_run;
-      __nv_bfloat16* orow =
-          O + (int64_t)(x.q0 + x.tok0 + tk) * p.o_st_tok + (int64_t)(x.kvh * G + (r % G)) * p.o_st_head;
-      // all 128 columns of the O row in one go, then O_h is released to the next item's
-      // PV_h(0) before the normalisation and the global stores
+      // this warp's O columns in one go, then O_h is released to the next item's PV_h(0)
+      // before the normalisation and the global stores
       uint32_t o[kD];
-      PATTN_TMEM_LD32(tO + 0, (o + 0));
-      PATTN_TMEM_LD32(tO + 32, (o + 32));
-      PATTN_TMEM_LD32(tO + 64, (o + 64));
-      PATTN_TMEM_LD32(tO + 96, (o + 96));
+#pragma unroll
+      for (int c0 = 0; c0 < kD; c0 += 32) PATTN_TMEM_LD32(tO + c0, (o + c0));
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(&bar.o_empty[h]);
@@ -640,18 +633,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       // each touch 32 different 128-B lines (rows are 256 B apart in `out`) -- those flooded
       // the MIO queue for ~4k clk per item and stalled the MMA warp's next S issue (trace).
       const int tk_last = h * bq_half + ((r | 31) / G);  // token of the warp's last row
-      if (p.k1_tma_store && tk_last < x.ntok) {
-        uint8_t* stg0 = smem + kOffStage + h * kStageHalf + (warp & 3) * kStageWarp;
+      const bool tma_out = p.k1_tma_store && tk_last < x.ntok;
+      uint8_t* stg0 = smem + kOffStage + (h * 4 + (warp & 3)) * kStageWarp;
+      if (tma_out) {
+        if (lane == 0) bulk_wait_group_read0();  // the slice's previous store has read it
+        __syncwarp();
+      }
+      const float inv = 1.f / l_run;
+      const uint64_t inv2 = f32x2(inv, inv);
+      if (tma_out) {
         const uint32_t row_off = (uint32_t)(r & 31) * 128;
-        const uint64_t inv2 = f32x2(inv, inv);
         const int tok_w = x.q0 + x.tok0 + h * bq_half + (r & ~31) / G;
 #pragma unroll
         for (int pass = 0; pass < 2; ++pass) {
           uint8_t* stg = stg0 + pass * 4096;
-          if (pass == 0) {
-            if (lane == 0) bulk_wait_group_read0();  // the slice's previous store has read it
-            __syncwarp();
-          }
 #pragma unroll
           for (int c = 0; c < 8; ++c) {
             const int c0 = pass * 64 + c * 8;
@@ -674,7 +669,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       } else if (row_valid) {
-        const uint64_t inv2 = f32x2(inv, inv);
+        __nv_bfloat16* orow = O + (int64_t)(x.q0 + x.tok0 + tk) * p.o_st_tok +
+                              (int64_t)(x.kvh * G + (r % G)) * p.o_st_head;
 #pragma unroll
         for (int c = 0; c < kD; c += 8) {
           uint4 v;
@@ -689,10 +685,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           *reinterpret_cast<uint4*>(orow + c) = v;
         }
       }
-      if (r == 0) PATTN_K1_TRACE(44 + h);
+      if (lead) PATTN_K1_TRACE(44 + h);
     }
     if (lane == 0) bulk_wait_group0();  // epilogue stores complete before the CTA retires
-    if (PATTN_K1_PP && h == 0) named_bar_sync(1, 256);  // drain half b's last hand-over
     if (threadIdx.x == 128) PATTN_CTA_END(k1, ic);
   }
 
@@ -707,11 +702,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 bool prefill_supported(const Params& p) {
   if (getenv("PATTN_DISABLE_K1")) return false;
   // BLOCK_Q = 256/G tokens split into two halves of 128 rows: G must divide 128
-  return p.D == kD && p.G >= 1 && p.G <= kHalfM && (kHalfM % p.G) == 0 && p.bs % 16 == 0 &&
+  // BLOCK_Q = 2 * floor(128 / G) tokens in two halves of 128 rows (padding rows when G does not
+  // divide 128, e.g. G = 3, 5, 6, 7, 12)
+  return p.D == kD && p.G >= 1 && p.G <= 64 && p.bs % 16 == 0 &&
          p.Hkv <= kMaxKvHeadMaps;
 }
 
-int prefill_block_q(int G) { return kM / G; }
+int prefill_block_q(int G) { return 2 * (kHalfM / G); }
 
 PrefillLaunch plan_prefill(const Params& p, int num_sms) {
   PrefillLaunch pl;

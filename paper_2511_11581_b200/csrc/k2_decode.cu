@@ -41,6 +41,11 @@ namespace pattn {
 namespace {
 
 constexpr int kSub = 16;  // keys per ring stage (one mma M tile)
+#ifdef PATTN_PARTITION_BLOCKIDX
+#define PATTN_PARTITION_BLOCKIDX_ON 1
+#else
+#define PATTN_PARTITION_BLOCKIDX_ON 0
+#endif
 constexpr int kItemRing = 16;
 #ifndef PATTN_K2_NP
 #define PATTN_K2_NP 4  // measured: per-SM decode rate +8% on 36 SMs vs 2 producers
@@ -105,6 +110,19 @@ __global__ void __launch_bounds__((NCW + kNP) * 32, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   PATTN_CTA_BEGIN(k2);
+  if (p.partition && !PATTN_PARTITION_BLOCKIDX_ON) {
+    // two-stream SM partition: the SMs with %smid < P belong to the prefill kernel K1 while it
+    // still has Q blocks to claim -- a decode CTA placed there first (graph replays launch the
+    // two branches in either order) leaves at once.  CTA 0 always works (progress guarantee).
+    __shared__ int s_leave;
+    if (threadIdx.x == 0) {
+      const int pre_left = *reinterpret_cast<volatile int*>(p.hdr + kHdrPrefillCounter) <
+                           p.hdr[kHdrTotalQBlocks] * p.Hkv;
+      s_leave = blockIdx.x != 0 && sm_id() < p.hdr[kHdrPrefillCtas] && pre_left;
+    }
+    __syncthreads();
+    if (s_leave) return;
+  }
   if (threadIdx.x == 0) {
     for (int s = 0; s < nst; ++s) {
       mbar_init(&full[s], 1);

@@ -24,14 +24,14 @@ namespace {
 // the additions is fixed, so the result is bitwise reproducible.
 constexpr int kMaxGroups = 4;
 
-template <int D>
+template <typename T, int D>
 __global__ void __launch_bounds__(64 * kMaxGroups) k3_reduce(Params p) {
   __shared__ float s_max[kMaxGroups][8];
   __shared__ float4 s_num[kMaxGroups][8][8];
   __shared__ float s_den[kMaxGroups][8];
   const int b = blockIdx.x;
   const int qb = p.cu_seqlens_q[b + 1] - p.cu_seqlens_q[b];
-  if (!(p.decode_to_k2 && qb == 1)) return;
+  if (!(p.decode_split && qb == 1)) return;
   const int c0 = p.cu_ch[b];
   const int n = p.cu_ch[b + 1] - c0;
   if (n <= 1) return;  // K2 wrote the final output itself
@@ -82,25 +82,34 @@ __global__ void __launch_bounds__(64 * kMaxGroups) k3_reduce(Params p) {
       dd += s_den[g][h];
     }
     const float inv = 1.f / dd;
-    uint2 packed;
-    packed.x = pack_bf16(t.x * inv, t.y * inv);
-    packed.y = pack_bf16(t.z * inv, t.w * inv);
-    __nv_bfloat16* O = static_cast<__nv_bfloat16*>(p.out);
-    *reinterpret_cast<uint2*>(O + (int64_t)tok * p.o_st_tok + (int64_t)(head0 + h) * p.o_st_head + d4g * 4) = packed;
+    T* O = static_cast<T*>(p.out) + (int64_t)tok * p.o_st_tok + (int64_t)(head0 + h) * p.o_st_head + d4g * 4;
+    if constexpr (sizeof(T) == 2) {
+      uint2 packed;
+      packed.x = pack_bf16(t.x * inv, t.y * inv);
+      packed.y = pack_bf16(t.z * inv, t.w * inv);
+      *reinterpret_cast<uint2*>(O) = packed;
+    } else {
+      *reinterpret_cast<float4*>(O) = make_float4(t.x * inv, t.y * inv, t.z * inv, t.w * inv);
+    }
   }
 }
 
 }  // namespace
 
-cudaError_t launch_reduce(const Params& p, cudaStream_t stream) {
+template <typename T>
+cudaError_t launch_reduce_t(const Params& p, cudaStream_t stream) {
   dim3 grid(p.B, p.Hkv * p.HG, p.D / 32);
   if (p.D == 64)
-    k3_reduce<64><<<grid, 64 * kMaxGroups, 0, stream>>>(p);
+    k3_reduce<T, 64><<<grid, 64 * kMaxGroups, 0, stream>>>(p);
   else if (p.D == 128)
-    k3_reduce<128><<<grid, 64 * kMaxGroups, 0, stream>>>(p);
+    k3_reduce<T, 128><<<grid, 64 * kMaxGroups, 0, stream>>>(p);
   else
     return cudaErrorInvalidValue;
   return cudaGetLastError();
+}
+
+cudaError_t launch_reduce(const Params& p, cudaStream_t stream) {
+  return p.dtype == 0 ? launch_reduce_t<float>(p, stream) : launch_reduce_t<__nv_bfloat16>(p, stream);
 }
 
 }  // namespace pattn

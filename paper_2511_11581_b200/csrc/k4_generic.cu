@@ -38,19 +38,42 @@ __global__ void __launch_bounds__(kWarps * 32) k4_generic(Params p) {
   T* __restrict__ O = static_cast<T*>(p.out);
 
   const int total_qb = p.hdr[kHdrTotalQBlocks];
-  const int n_items = total_qb * p.Hkv;
+  const int n_pre = total_qb * p.Hkv;
+  // decode segments (split-KV) when the decode kernel K2 cannot take them: one item
+  // per (segment, KV head) covering the G query heads of that KV head
+  const int n_items = n_pre + (p.k4_decodes ? p.hdr[kHdrTotalChunks] * p.Hkv : 0);
   for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-    const int j = total_qb - 1 - it / p.Hkv;  // global Q-block id, last first
-    const int kvh = it % p.Hkv;
-    const int b = upper_bound_minus1(p.cu_qb, p.B, j);  // App. B P:46 binary search
-    const int qblk = j - p.cu_qb[b];
-    const int q0 = p.cu_seqlens_q[b];
-    const int qlen = p.cu_seqlens_q[b + 1] - q0;
-    const int L = p.seq_lens[b];
-    const int ctx = L - qlen;
-    const int tok0 = qblk * BQ;
-    const int ntok = min(BQ, qlen - tok0);
-    const int kv_end = ctx + tok0 + ntok;  // keys visible to the last row of the block
+    int b, kvh, q0, ntok, tok0, ctx, kv_begin, kv_end, nseg = 1, chunk = 0;
+    if (it < n_pre) {
+      const int j = total_qb - 1 - it / p.Hkv;  // global Q-block id, last first
+      kvh = it % p.Hkv;
+      b = upper_bound_minus1(p.cu_qb, p.B, j);  // App. B P:46 binary search
+      const int qblk = j - p.cu_qb[b];
+      q0 = p.cu_seqlens_q[b];
+      const int qlen = p.cu_seqlens_q[b + 1] - q0;
+      ctx = p.seq_lens[b] - qlen;
+      tok0 = qblk * BQ;
+      ntok = min(BQ, qlen - tok0);
+      kv_begin = 0;
+      kv_end = ctx + tok0 + ntok;  // keys visible to the last row of the block
+    } else {
+      const int u = it - n_pre;
+      chunk = u / p.Hkv;
+      kvh = u - chunk * p.Hkv;
+      b = upper_bound_minus1(p.cu_ch, p.B, chunk);
+      const int c0 = p.cu_ch[b];
+      nseg = p.cu_ch[b + 1] - c0;
+      const int L = p.seq_lens[b];
+      const int nblk = (L + p.bs - 1) / p.bs;
+      const int per = (nblk + nseg - 1) / nseg;  // K5's equal block ranges (reading R9)
+      const int kb0 = (chunk - c0) * per;
+      q0 = p.cu_seqlens_q[b];
+      ctx = L - 1;
+      tok0 = 0;
+      ntok = 1;
+      kv_begin = min(kb0 * p.bs, L);
+      kv_end = min((kb0 + per) * p.bs, L);
+    }
     const int32_t* bt = p.block_table + (int64_t)b * p.bt_stride;
 
     __syncthreads();  // previous item finished with sQ
@@ -74,7 +97,7 @@ __global__ void __launch_bounds__(kWarps * 32) k4_generic(Params p) {
       for (int k = 0; k < DV; ++k) acc[i][k] = 0.f;
     }
 
-    for (int t0 = 0; t0 < kv_end; t0 += kTileKeys) {
+    for (int t0 = kv_begin; t0 < kv_end; t0 += kTileKeys) {
       __syncthreads();
       for (int idx = threadIdx.x; idx < kTileKeys * D; idx += kWarps * 32) {
         int jj = idx / D, d = idx - jj * D;
@@ -97,7 +120,7 @@ __global__ void __launch_bounds__(kWarps * 32) k4_generic(Params p) {
         if (r >= BM) break;
         const int tk = r / G;
         if (tk >= ntok) continue;
-        const int row_end = ctx + tok0 + tk + 1;  // keys 0 .. ctx+i (self-inclusive)
+        const int row_end = min(ctx + tok0 + tk + 1, kv_end);  // keys 0 .. ctx+i (self-inclusive)
         if (t0 >= row_end) continue;              // warp-uniform
         const int t = t0 + lane;
         float s = -INFINITY;
@@ -133,6 +156,18 @@ __global__ void __launch_bounds__(kWarps * 32) k4_generic(Params p) {
       const int tk = r / G;
       if (tk >= ntok) continue;
       const int h = kvh * G + (r - tk * G);
+      if (nseg > 1) {
+        // partial (m, l, acc) of this segment for K3; m in the log2 domain;
+        // an empty segment leaves m = -inf, l = 0, acc = 0 (skipped by the merge)
+        const int64_t row = (int64_t)chunk * p.Hq + h;
+        if (lane == 0) {
+          p.part_m[row] = m[i];
+          p.part_l[row] = l[i];
+        }
+#pragma unroll
+        for (int k = 0; k < DV; ++k) p.part_acc[row * D + lane + 32 * k] = acc[i][k];
+        continue;
+      }
       T* o = O + (int64_t)(q0 + tok0 + tk) * p.o_st_tok + (int64_t)h * p.o_st_head;
       const float inv = 1.f / l[i];
 #pragma unroll

@@ -1,9 +1,9 @@
 // K5 -- device batch metadata (§6.1 "Computation of Metadata").
 //
 // From cu_seqlens_q and seq_lens (device-resident, no host sync) one CTA computes:
-//   * per sequence b: q_b, L_b and its class -- "decode" (q_b == 1, routed to the
-//     split-KV decode kernel K2 when decode_to_k2; reading R15) or "Q-block" (every
-//     other non-empty sequence, routed to K1/K4);
+//   * per sequence b: q_b, L_b and its class -- "decode" (q_b == 1: split-KV decode units
+//     of K2, or of K4 for fp32 / block sizes K2 cannot fetch; reading R15) or "Q-block"
+//     (every other non-empty sequence, routed to K1/K4);
 //   * cu_q_blocks: exclusive scan of ceil(q_b / BLOCK_Q) over Q-block sequences
 //      -- the total Q-block count is its last entry;
 //   * the number of decodes and the decode segment plan: segment cap
@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(kMaxThreads) k5_metadata(Params p) {
     q0 = qb;
     L0 = L;
     my_viol += qb > p.max_query_len_hint ? 1ull : 0ull;  // the host planned with a smaller bound
-    if (p.decode_to_k2 && qb == 1) {
+    if (p.decode_split && qb == 1) {
       my_dec += 1;
       my_blocks += (unsigned long long)((L + p.bs - 1) / p.bs);
       my_keys += (unsigned long long)L;
@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(kMaxThreads) k5_metadata(Params p) {
     keys = block_sum_u64(my_keys, s_red);
   }
 
-  const long long units = (long long)p.Hkv * p.HG;
+  const long long units = p.k4_decodes ? (long long)p.Hkv : (long long)p.Hkv * p.HG;  // items per segment
   long long C;
   if (p.split_mode == 1) {
     C = INT_MAX;
@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(kMaxThreads) k5_metadata(Params p) {
         qb = __ldg(p.cu_seqlens_q + b + 1) - __ldg(p.cu_seqlens_q + b);
         L = __ldg(p.seq_lens + b);
       }
-      if (p.decode_to_k2 && qb == 1) {
+      if (p.decode_split && qb == 1) {
         const long long nblk = (L + p.bs - 1) / p.bs;
         cnt.y = (int)((nblk + C - 1) / C);
       } else if (qb > 0) {

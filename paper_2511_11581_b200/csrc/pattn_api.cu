@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <new>
 #include <mutex>
 #include <utility>
 #include <vector>
@@ -164,6 +165,7 @@ pattn_tuning_t resolve_tuning(const pattn_problem_t* p) {
 
 struct Plan {
   bool use_k1 = false, use_k2 = false, use_k4 = false, use_k7 = false;
+  bool k4_decodes = false;  // decode segments on K4 (when K2 cannot take them)
   int block_q = 1, HG = 1, rpw = 8;
   int target_items = 0, min_chunk = 1, split_mode = 0, max_chunks = 0;
   int num_sms = 148;
@@ -207,7 +209,8 @@ void fill_params(const pattn_problem_t* p, const Plan& pl, Params* k) {
   k->block_q = pl.block_q;
   k->HG = pl.HG;
   k->max_chunks = pl.max_chunks;
-  k->decode_to_k2 = pl.use_k2 ? 1 : 0;
+  k->decode_split = (pl.use_k2 || pl.k4_decodes) ? 1 : 0;
+  k->k4_decodes = pl.k4_decodes ? 1 : 0;
   k->split_mode = pl.split_mode;
   k->target_items = pl.target_items;
   k->min_chunk_blocks = pl.min_chunk;
@@ -265,6 +268,14 @@ pattn_status_t make_plan(const pattn_problem_t* p, const void* q, const void* kc
     pl->block_q = G <= 32 ? std::max(1, 32 / G) : 1;
     pl->use_k4 = maybe_prefill && !pl->use_k7;
   }
+  // No K2 (fp32, block sizes that are not a multiple of 16, unaligned strides): K4 runs the
+  // decodes as split-KV segment units too (parallel tiled softmax on the SIMT path), merged by K3
+  // (K3 stores 16-byte vectors: output rows must be 16-byte aligned, else decodes stay unsplit)
+  const int64_t esz = bf16 ? 2 : 4;
+  const bool o_vec = (p->o_stride_tok * esz) % 16 == 0 && (p->o_stride_head * esz) % 16 == 0 &&
+                     (out == nullptr || aligned16(out));
+  pl->k4_decodes = !pl->use_k2 && !pl->use_k7 && o_vec;
+  if (pl->k4_decodes) pl->use_k4 = true;
   const int bm = pl->block_q * G;
   pl->rpw = bm <= 32 ? 8 : 16;
 
@@ -285,7 +296,10 @@ pattn_status_t make_plan(const pattn_problem_t* p, const void* q, const void* kc
   if (pl->target_items < 1) pl->target_items = 1;
   if (pl->min_chunk < 1) pl->min_chunk = 1;
   const long long units = (long long)p->num_kv_heads * pl->HG;
-  pl->max_chunks = pl->use_k2 ? (int)(p->num_seqs + (pl->target_items + units - 1) / units + 1) : 0;
+  const long long seg_units = pl->k4_decodes ? (long long)p->num_kv_heads : units;  // K4: all G heads per item
+  pl->max_chunks = (pl->use_k2 || pl->k4_decodes)
+                       ? (int)(p->num_seqs + (pl->target_items + seg_units - 1) / seg_units + 1)
+                       : 0;
 
   // workspace layout
   size_t off = 0;
@@ -307,7 +321,7 @@ pattn_status_t make_plan(const pattn_problem_t* p, const void* q, const void* kc
   // grids
   if (pl->use_k4) {
     const int ctas_per_sm = 4;
-    const long long max_items = (long long)std::max(1, p->num_tokens) * p->num_kv_heads;
+    const long long max_items = ((long long)std::max(1, p->num_tokens) + pl->max_chunks) * p->num_kv_heads;
     pl->k4_grid = (int)std::min<long long>(max_items, (long long)pl->num_sms * ctas_per_sm);
     if (pl->k4_grid < 1) pl->k4_grid = 1;
   }
@@ -562,13 +576,15 @@ pattn_status_t run(const pattn_problem_t* p, const void* q, const void* k_cache,
   }
   if (pl.use_k7) step(PATTN_KERNEL_BASELINE, s1, [&] { return launch_baseline(k, s1); });
   if (pl.use_k4) step(PATTN_KERNEL_GENERIC, s1, [&] { return launch_generic(k, pl.k4_grid, pl.rpw, s1); });
+  if (pl.k4_decodes) step(PATTN_KERNEL_REDUCE, s1, [&] { return launch_reduce(k, s1); });
   if (two) {
     cudaError_t ej = cudaEventRecord(fj.join, s2);
     if (ej == cudaSuccess) ej = cudaStreamWaitEvent(s1, fj.join, 0);
     if (e == cudaSuccess) e = ej;
   }
   if (e != cudaSuccess) return cuda_fail(e);
-  if (debug_sync()) {
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (debug_sync() && cudaStreamIsCapturing(s1, &cap) == cudaSuccess && cap == cudaStreamCaptureStatusNone) {
     // PATTN_DEBUG_SYNC=1: synchronise and check what the device saw against the host hints
     // (a max_query_len hint below the true maximum can drop the prefill kernel from the plan)
     int32_t viol = 0;
@@ -745,8 +761,8 @@ pattn_status_t pattn_debug_plan(const pattn_problem_t* p, const int32_t* cu_seql
 int32_t pattn_planned_launches(const pattn_problem_t* p) {
   Plan pl;
   if (make_plan(p, nullptr, nullptr, nullptr, nullptr, &pl) != PATTN_OK) return 0;
-  return 1 + (pl.use_k1 ? 1 : 0) + (pl.use_k4 ? 1 : 0) + (pl.use_k7 ? 1 : 0) +
-         (pl.use_k2 ? 2 : 0);
+  return 1 + (pl.use_k1 ? 1 : 0) + (pl.use_k4 ? 1 : 0) + (pl.use_k7 ? 1 : 0) + (pl.use_k2 ? 2 : 0) +
+         (pl.k4_decodes ? 1 : 0);
 }
 
 int32_t pattn_planned_kernels(const pattn_problem_t* p) {
@@ -754,6 +770,7 @@ int32_t pattn_planned_kernels(const pattn_problem_t* p) {
   if (make_plan(p, nullptr, nullptr, nullptr, nullptr, &pl) != PATTN_OK) return 0;
   return (1 << PATTN_KERNEL_METADATA) | (pl.use_k1 ? 1 << PATTN_KERNEL_PREFILL : 0) |
          (pl.use_k2 ? (1 << PATTN_KERNEL_DECODE) | (1 << PATTN_KERNEL_REDUCE) : 0) |
+         (pl.k4_decodes ? (1 << PATTN_KERNEL_REDUCE) : 0) |
          (pl.use_k4 ? 1 << PATTN_KERNEL_GENERIC : 0) | (pl.use_k7 ? 1 << PATTN_KERNEL_BASELINE : 0);
 }
 
@@ -827,6 +844,77 @@ pattn_status_t pattn_plan_tuning(const pattn_problem_t* p, pattn_tuning_t* out) 
   if (st != PATTN_OK) return st;
   *out = resolve_tuning(p);
   return PATTN_OK;
+}
+
+struct pattn_graph {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+};
+
+pattn_status_t pattn_graph_capture(const pattn_problem_t* p, const void* q, const void* k_cache, const void* v_cache,
+                                   const int32_t* block_table, const int32_t* cu_seqlens_q, const int32_t* seq_lens,
+                                   float scale, void* out, void* workspace, size_t workspace_bytes, void* stream,
+                                   void* stream2, pattn_graph_t* graph) {
+  if (!graph || !stream) return PATTN_ERR_INVALID_ARG;  // capture needs a real (non-legacy) stream
+  *graph = nullptr;
+  {
+    // host-detectable errors first, before any capture is begun
+    Plan pl;
+    pattn_status_t st = make_plan(p, q, k_cache, v_cache, out, &pl);
+    if (st == PATTN_OK)
+      st = check_call(p, pl, q, k_cache, v_cache, block_table, cu_seqlens_q, seq_lens, scale, out, workspace,
+                      workspace_bytes);
+    if (st != PATTN_OK) return st;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
+  if (e != cudaSuccess) return cuda_fail(e);
+  pattn_exec_opts_t o;
+  memset(&o, 0, sizeof(o));
+  o.stream2 = stream2;
+  const pattn_status_t st = run(p, q, k_cache, v_cache, block_table, cu_seqlens_q, seq_lens, scale, out, workspace,
+                                workspace_bytes, stream, &o, false);
+  cudaGraph_t g = nullptr;
+  e = cudaStreamEndCapture(s, &g);  // always end the capture, also after a failed enqueue
+  if (st != PATTN_OK) {
+    if (g) cudaGraphDestroy(g);
+    return st;
+  }
+  if (e != cudaSuccess) return cuda_fail(e);
+  cudaGraphExec_t x = nullptr;
+  e = cudaGraphInstantiateWithFlags(&x, g, 0);
+  if (e != cudaSuccess) {
+    cudaGraphDestroy(g);
+    return cuda_fail(e);
+  }
+  pattn_graph* h = new (std::nothrow) pattn_graph;
+  if (!h) {
+    cudaGraphExecDestroy(x);
+    cudaGraphDestroy(g);
+    return PATTN_ERR_INVALID_ARG;
+  }
+  h->graph = g;
+  h->exec = x;
+  *graph = h;
+  return PATTN_OK;
+}
+
+pattn_status_t pattn_graph_launch(pattn_graph_t graph, void* stream) {
+  if (!graph || !graph->exec) return PATTN_ERR_INVALID_ARG;
+  const cudaError_t e = cudaGraphLaunch(graph->exec, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? PATTN_OK : cuda_fail(e);
+}
+
+pattn_status_t pattn_graph_destroy(pattn_graph_t graph) {
+  if (!graph) return PATTN_ERR_INVALID_ARG;
+  cudaError_t e = cudaSuccess;
+  if (graph->exec) e = cudaGraphExecDestroy(graph->exec);
+  if (graph->graph) {
+    const cudaError_t e2 = cudaGraphDestroy(graph->graph);
+    if (e == cudaSuccess) e = e2;
+  }
+  delete graph;
+  return e == cudaSuccess ? PATTN_OK : cuda_fail(e);
 }
 
 int32_t pattn_version(void) { return kVersion; }

@@ -91,6 +91,9 @@ EXPORTS = [
     "pattn_write_kv",
     "pattn_set_tuning_tree",
     "pattn_plan_tuning",
+    "pattn_graph_capture",
+    "pattn_graph_launch",
+    "pattn_graph_destroy",
 ]
 
 
@@ -133,6 +136,13 @@ def load() -> ctypes.CDLL:
                 lib.pattn_set_tuning_tree.argtypes = [vp, ctypes.c_int32]
                 lib.pattn_plan_tuning.restype = ctypes.c_int
                 lib.pattn_plan_tuning.argtypes = [P, vp]
+            if hasattr(lib, "pattn_graph_capture"):  # absent only in older A/B builds
+                lib.pattn_graph_capture.restype = ctypes.c_int
+                lib.pattn_graph_capture.argtypes = common + [vp, ctypes.POINTER(vp)]
+                lib.pattn_graph_launch.restype = ctypes.c_int
+                lib.pattn_graph_launch.argtypes = [vp, vp]
+                lib.pattn_graph_destroy.restype = ctypes.c_int
+                lib.pattn_graph_destroy.argtypes = [vp]
             lib.pattn_version.restype = ctypes.c_int32
             lib.pattn_last_error.restype = ctypes.c_char_p
             _lib = lib
@@ -384,6 +394,52 @@ def unified_attention_hostio(
         "pattn_unified_attention_hostio",
     )
     return out_host
+
+
+class Graph:
+    """A captured unified call (pattn_graph_capture): replay with launch(); the tensors given
+    at capture are baked in -- refresh their contents between launches."""
+
+    def __init__(self, handle: int, keep: tuple):
+        self.handle = handle
+        self._keep = keep  # the captured buffers must outlive the graph
+
+    def launch(self, stream: Optional[torch.cuda.Stream] = None):
+        s = stream if stream is not None else torch.cuda.current_stream()
+        _check(load().pattn_graph_launch(self.handle, s.cuda_stream), "pattn_graph_launch")
+
+    def close(self):
+        if self.handle:
+            _check(load().pattn_graph_destroy(self.handle), "pattn_graph_destroy")
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def graph_capture(q, k_cache, v_cache, block_table, cu_seqlens_q, seq_lens, scale, num_kv_heads, block_size, out,
+                  workspace, *, kv_layout="NHD", max_query_len=None, max_seq_len=None, flags=0,
+                  stream: Optional[torch.cuda.Stream] = None, stream2: Optional[torch.cuda.Stream] = None) -> Graph:
+    """Capture one unified call on the given (persistent) buffers into a CUDA graph (PAPER.md
+    §6.2).  `workspace` is required: it is baked into the graph."""
+    lib = load()
+    _validate(q, k_cache, v_cache, block_table, cu_seqlens_q, seq_lens, out, kv_layout)
+    p = make_problem(q, k_cache, num_kv_heads, block_size, block_table, seq_lens.shape[0], out, kv_layout,
+                     max_query_len, max_seq_len, flags)
+    need = workspace_size(p)
+    if workspace.numel() < need:
+        raise PattnError(6, f"workspace of {workspace.numel()} bytes < {need}")
+    s = stream if stream is not None else torch.cuda.Stream(q.device)
+    h = ctypes.c_void_p()
+    _check(lib.pattn_graph_capture(
+        ctypes.byref(p), q.data_ptr(), k_cache.data_ptr(), v_cache.data_ptr(), block_table.data_ptr(),
+        cu_seqlens_q.data_ptr(), seq_lens.data_ptr(), ctypes.c_float(scale), out.data_ptr(), workspace.data_ptr(),
+        workspace.numel(), s.cuda_stream, stream2.cuda_stream if stream2 is not None else None, ctypes.byref(h)),
+        "pattn_graph_capture")
+    return Graph(h.value, (q, k_cache, v_cache, block_table, cu_seqlens_q, seq_lens, out, workspace, s, stream2))
 
 
 def write_kv(

@@ -94,10 +94,15 @@ class LocalBatch:
 
 def local_batch(plan: ShardPlan, rank: int, q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor,
                 block_table: np.ndarray, cu_seqlens_q: np.ndarray, seq_lens: np.ndarray, block_size: int,
-                device: Optional[torch.device] = None) -> LocalBatch:
-    """Build rank `rank`'s local inputs from global ones (NHD caches).  Mode "seq": the rank's
-    sequences, their blocks gathered into a compact local cache and the block table renumbered
-    0..n-1.  Mode "kvhead": the rank's KV-head slice of the caches and query-head slice of q."""
+                device: Optional[torch.device] = None, kv_layout: str = "NHD") -> LocalBatch:
+    """Build rank `rank`'s local inputs from global ones.  Caches are NHD
+    [num_blocks, block_size, Hkv, D] or HND [num_blocks, Hkv, block_size, D] (`kv_layout`).
+    Mode "seq": the rank's sequences, their blocks gathered into a compact local cache and the
+    block table renumbered 0..n-1.  Mode "kvhead": the rank's KV-head slice of the caches and
+    query-head slice of q."""
+    if kv_layout not in ("NHD", "HND"):
+        raise ValueError(kv_layout)
+    head_axis = 2 if kv_layout == "NHD" else 1
     dev = device if device is not None else q.device
     cu = np.asarray(cu_seqlens_q, np.int64)
     sl = np.asarray(seq_lens, np.int64)
@@ -106,8 +111,8 @@ def local_batch(plan: ShardPlan, rank: int, q: torch.Tensor, k_cache: torch.Tens
         kvh, qh = plan.kv_heads[rank], plan.q_heads[rank]
         return LocalBatch(
             q=q[:, qh.start:qh.stop].contiguous().to(dev),
-            k_cache=k_cache[:, :, kvh.start:kvh.stop].contiguous().to(dev),
-            v_cache=v_cache[:, :, kvh.start:kvh.stop].contiguous().to(dev),
+            k_cache=k_cache.narrow(head_axis, kvh.start, len(kvh)).contiguous().to(dev),
+            v_cache=v_cache.narrow(head_axis, kvh.start, len(kvh)).contiguous().to(dev),
             block_table=torch.from_numpy(bt.astype(np.int32)).to(dev),
             cu_seqlens_q=torch.from_numpy(cu.astype(np.int32)).to(dev),
             seq_lens=torch.from_numpy(sl.astype(np.int32)).to(dev),
@@ -137,7 +142,7 @@ def local_batch(plan: ShardPlan, rank: int, q: torch.Tensor, k_cache: torch.Tens
         cu_seqlens_q=torch.from_numpy(lcu).to(dev),
         seq_lens=torch.from_numpy(sl[ids].astype(np.int32)).to(dev),
         token_ids=tok,
-        num_kv_heads=k_cache.shape[2],
+        num_kv_heads=k_cache.shape[head_axis],
         q_heads=range(q.shape[1]),
     )
 

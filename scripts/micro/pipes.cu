@@ -23,6 +23,8 @@ __global__ void k(float* out, int iters, long long* clk) {
       if (OP == 6) asm volatile("add.rn.f32x2 %0, %0, %0;" : "+l"(v2[i]));
       if (OP == 7) { asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(a[i])); asm volatile("fma.rn.f32x2 %0, %0, %0, %0;" : "+l"(v2[i])); }
       if (OP == 3) asm volatile("fma.rn.f32 %0, %0, %0, %0;" : "+f"(a[i]));
+      if (OP == 8) { uint32_t r; asm volatile("prmt.b32 %0, %1, %2, 0x7632;" : "=r"(r) : "r"(__float_as_uint(a[i])), "r"(u[i])); a[i] = __uint_as_float(r); }
+      if (OP == 9) { asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(a[i])); uint32_t r; asm volatile("prmt.b32 %0, %1, %2, 0x7632;" : "=r"(r) : "r"(u[(i + 8) & 15]), "r"(u[i])); u[i] ^= r; }
     }
   }
   unsigned long long t1 = clock64();
@@ -42,6 +44,6 @@ template <int OP> void run(const char* name, int warps) {
   cudaFree(o); cudaFree(c);
 }
 int main() {
-  for (int w : {8, 16}) { run<0>("ex2", w); run<2>("ffma2", w); run<6>("fadd2", w); run<7>("ex2+ffma2", w); run<3>("ffma", w); }
+  for (int w : {4, 8, 16}) { run<0>("ex2", w); run<1>("f2fp", w); run<5>("ex2+f2fp", w); run<8>("prmt", w); run<9>("ex2+prmt", w); run<2>("ffma2", w); run<7>("ex2+ffma2", w); }
   return 0;
 }

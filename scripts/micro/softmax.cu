@@ -45,10 +45,11 @@ __global__ void k(const float* in, uint32_t* out, int tiles, long long* clk) {
       const uint64_t xx = ffma2(f2(s[c], s[c + 1]), ca2, nb2);
       uint64_t ee;
       float e0, e1;
-      if (((c >> 1) & MASK) == MASK && MASK < 64) { ee = poly2(xx); e0 = lo(ee); e1 = hi(ee); }
+      if (((c >> 1) & MASK) == MASK && MASK < 64 && MASK != 254) { ee = poly2(xx); e0 = lo(ee); e1 = hi(ee); }
       else { e0 = ex2(lo(xx)); e1 = ex2(hi(xx)); ee = f2(e0, e1); }
       rs2[(c >> 1) & 3] = fadd2(rs2[(c >> 1) & 3], ee);
-      p[c >> 1] = pk(e0, e1);
+      if (MASK == 254) p[c >> 1] = __byte_perm(__float_as_uint(e0), __float_as_uint(e1), 0x7632);
+      else p[c >> 1] = pk(e0, e1);
     }
     const uint64_t rr = fadd2(fadd2(rs2[0], rs2[1]), fadd2(rs2[2], rs2[3]));
     l_run = l_run + lo(rr) + hi(rr);
@@ -73,6 +74,6 @@ template <int MASK> void run(int warps) {
   printf("mask %3d warps/SM %2d (%d per SMSP): %.0f clk per tile per warp\n", MASK, warps, warps / 4, (double)h / tiles);
 }
 int main() {
-  for (int w : {4, 8, 16}) { run<255>(w); run<7>(w); run<3>(w); run<1>(w); }
+  for (int w : {4, 8, 16}) { run<255>(w); run<254>(w); run<7>(w); }
   return 0;
 }

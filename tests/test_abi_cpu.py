@@ -80,9 +80,11 @@ def test_validate_metadata_host_matches_oracle_codes(lib):
 
 def test_workspace_and_planned_launches(lib, monkeypatch):
     so = lib.load()
-    p = _problem(lib)  # fp32 -> metadata + generic
+    p = _problem(lib)  # fp32 -> metadata + generic (Q blocks + split decode segments) + reduce
     assert so.pattn_workspace_size(ctypes.byref(p)) > 0
-    assert lib.planned_launches(p) == 2
+    assert lib.planned_launches(p) == 3
+    assert lib.planned_kernels(p) == (1 << lib.KERNEL_METADATA) | (1 << lib.KERNEL_GENERIC) | (
+        1 << lib.KERNEL_REDUCE)
     pb = _problem(lib, Hq=32, Hkv=8, D=128, dtype=1, T=64, B=64, nb=16448, maxb=257)
     pb.max_query_len = 1
     assert lib.planned_launches(pb) == 3  # metadata + decode + reduce
@@ -91,7 +93,7 @@ def test_workspace_and_planned_launches(lib, monkeypatch):
     pb.max_query_len = 2048
     assert lib.planned_launches(pb) == 4  # + the Q-block kernel
     pb.flags = lib.FLAG_FORCE_GENERIC
-    assert lib.planned_launches(pb) == 2
+    assert lib.planned_launches(pb) == 3
     bad = _problem(lib, D=96)
     assert so.pattn_workspace_size(ctypes.byref(bad)) == 0
     assert so.pattn_hostio_workspace_size(ctypes.byref(p)) > so.pattn_workspace_size(ctypes.byref(p))

@@ -98,6 +98,12 @@ PREFILL_CASES = [
     (((3, 200), (0, 47)), (16, 1), 32, "NHD"),
     (((0, 300),), (8, 8), 16, "NHD"),       # G = 1: BLOCK_Q = 128
     (((0, 257), (9, 9)), (128, 2), 128, "NHD"),  # G = 64: BLOCK_Q = 2; bs 128 = one block per tile
+    # G not dividing 128 (common GQA ratios): BLOCK_Q = 2 * floor(128 / G), padding rows per half
+    (((0, 700), (300, 90), (5, 1)), (48, 8), 16, "NHD"),   # G = 6 (21 tokens x 6 = 126 rows per half)
+    (((0, 500), (64, 130)), (28, 4), 16, "HND"),           # G = 7 (Qwen-style 28q/4kv)
+    (((0, 333), (17, 40)), (96, 8), 32, "NHD"),            # G = 12 (10 tokens x 12 = 120 rows)
+    (((0, 290),), (15, 5), 16, "NHD"),                     # G = 3 (42 x 3 = 126)
+    (((0, 260), (100, 33)), (40, 8), 48, "NHD"),           # G = 5 (25 x 5 = 125)
 ]
 
 
@@ -105,6 +111,11 @@ PREFILL_CASES = [
 def test_prefill_tensor_core_path(case):
     seqs, heads, bs, layout = PREFILL_CASES[case]
     w = Workload(f"prefill{case}", seqs, heads[0], heads[1], 128, bs, "bf16")
+    kv = np.zeros((1, bs, heads[1], 128), np.uint16)
+    p = P.make_problem(torch.zeros((1, heads[0], 128), dtype=torch.bfloat16, device="cuda"),
+                       torch.zeros(kv.shape, dtype=torch.bfloat16, device="cuda"), heads[1], bs,
+                       torch.zeros((1, 1), dtype=torch.int32, device="cuda"), 1, max_query_len=64)
+    assert P.planned_kernels(p) & (1 << P.KERNEL_PREFILL), "not on the tcgen05 prefill kernel"  # K1, not K4
     batch = generate(w, seed=100 + case, dist="peaked", layout=layout)
     _check(batch, 0, f"prefill case {case}")
 
@@ -156,9 +167,8 @@ def test_debug_plan_bit_exact():
             plan = P.debug_plan(prob, db.cu, db.sl).cpu().numpy()
             B = w.num_seqs
             block_q = int(plan[3])
-            generic = bool(flags & P.FLAG_FORCE_GENERIC)
             qlens = np.diff(batch.cu_seqlens_q)
-            dec = (qlens == 1) & (not generic)
+            dec = qlens == 1  # decode units on K2, or split on K4 (FORCE_GENERIC)
             # Q-block kernel sequences: everything not routed to the decode kernel
             cu_qb_ref = M.build_batch_meta(np.concatenate([[0], np.cumsum(np.where(dec, 0, qlens))]),
                                            np.where(dec, 0, batch.seq_lens), block_q)["cu_q_blocks"]
@@ -362,6 +372,26 @@ def test_segment_reduce_groups_follow_segment_count(flags):
     assert torch.equal(db.run(flags=flags), a)
 
 
+@pytest.mark.parametrize("dt,bs,layout", [("bf16", 7, "NHD"), ("f32", 16, "HND"), ("f32", 5, "NHD"), ("bf16", 24, "HND")])
+@pytest.mark.parametrize("flags", [0, 0x4])
+def test_split_decode_on_generic_path(dt, bs, layout, flags):
+    """Block sizes K2 cannot fetch (not a multiple of 16) and the fp32 path: decodes still run
+    as split-KV segments (parallel tiled softmax) -- on the SIMT kernel K4 -- and K3
+    merges them; long contexts get many segments."""
+    w = Workload("k4split", ((20000, 1), (0, 70), (3000, 1), (17, 1), (700, 40), (9000, 1)), 32, 8, 128, bs, dt)
+    batch = generate(w, seed=17, dist="peaked", poison=True, layout=layout)
+    db = DeviceBatch(batch)
+    p = P.make_problem(db.q, db.k, w.num_kv_heads, w.block_size, db.bt, w.num_seqs, None, layout, 70, 20001, flags)
+    assert P.planned_kernels(p) == (1 << P.KERNEL_METADATA) | (1 << P.KERNEL_GENERIC) | (1 << P.KERNEL_REDUCE)
+    plan = P.debug_plan(p, db.cu, db.sl).cpu().numpy()
+    B = w.num_seqs
+    nch = np.diff(plan[8 + B + 1: 8 + 2 * B + 2])
+    assert nch[0] > 1  # the 20k-token decode is split
+    a = db.run(flags=flags).clone()
+    assert_close(out_f64(a), O.batch_attention(batch), dt, f"K4 split decode {dt} bs={bs} flags={flags}")
+    assert torch.equal(db.run(flags=flags), a)
+
+
 def test_hintless_call_matches_oracle():
     """No host hints (max_query_len / max_seq_len = 0): the planner uses its upper bounds."""
     w = Workload("nohint", ((0, 300), (2500, 1), (64, 40), (900, 1)), 32, 8, 128, 16, "bf16")
@@ -453,3 +483,45 @@ def test_baseline_kernel_parity(case):
 
 def test_baseline_kernel_config1_fp32():
     _check(generate(CONFIGS["c1_tiny"], seed=1001), P.FLAG_BASELINE, "baseline c1")
+
+
+# ---------------------------------------------------------------- CUDA-graph buckets (NEXT-1)
+@pytest.mark.parametrize("two_streams", [False, True])
+def test_graph_bucket_replays_with_fewer_sequences(two_streams):
+    """Graphs recorded once per batch-size bucket (§6.2) and replayed for
+    batches smaller than the bucket: padding sequences have q_b = 0, L_b = 0.  Decode-only
+    buckets and a mixed bucket (prefill + decode, two streams), against the oracle."""
+    from paper_2511_11581_b200.graphs import GraphBuckets
+
+    # one KV cache holding every sequence the batches below use
+    seqs = ((3000, 1), (100, 1), (4096, 1), (17, 1), (900, 1), (2500, 1), (0, 1))
+    w = Workload("graphdec", seqs, 32, 8, 128, 16, "bf16")
+    batch = generate(w, seed=41, dist="peaked", poison=True)
+    db = DeviceBatch(batch)
+    gb = GraphBuckets(db.k, db.v, 32, 8, 16, w.scale, buckets=(4, 8), max_query_len=1, max_seq_len=4097,
+                      two_streams=two_streams)
+    ref = O.batch_attention(batch)
+    for ids in ([0, 1, 2, 3, 4], [5, 6, 1], [2]):  # bucket 8, bucket 4, bucket 4
+        ids = np.array(ids)
+        q = db.q[torch.from_numpy(ids).cuda()]
+        bt = db.bt[torch.from_numpy(ids).cuda()]
+        sl = db.sl[torch.from_numpy(ids).cuda()]
+        cu = torch.arange(len(ids) + 1, dtype=torch.int32, device="cuda")
+        out = gb.run(q, bt, cu, sl).clone()
+        torch.cuda.synchronize()
+        assert_close(out_f64(out), ref[ids], "bf16", f"graph bucket ids={ids.tolist()}")
+        again = gb.run(q, bt, cu, sl)
+        torch.cuda.synchronize()
+        assert torch.equal(again, out)
+    gb.close()
+
+    # mixed bucket: up to 8 sequences, 400 query tokens (prefills + decodes), two streams
+    w = Workload("graphmix", ((0, 200), (3000, 1), (64, 100), (900, 1), (1500, 1)), 32, 8, 128, 16, "bf16")
+    batch = generate(w, seed=42, dist="peaked", poison=True)
+    db = DeviceBatch(batch)
+    gb = GraphBuckets(db.k, db.v, 32, 8, 16, w.scale, buckets=(8,), max_query_len=256, max_seq_len=3001,
+                      token_capacity={8: 400}, two_streams=two_streams)
+    out = gb.run(db.q, db.bt, db.cu, db.sl).clone()
+    torch.cuda.synchronize()
+    assert_close(out_f64(out), O.batch_attention(batch), "bf16", "graph mixed bucket")
+    gb.close()

@@ -216,3 +216,23 @@ def test_validate_codes():
     assert O.validate(cu, sl, 4, 3, bt) == 0
     assert O.validate(cu, np.array([2, 5], np.int32), 4, 3, bt) == 3  # q_b > L_b
     assert O.validate(cu, sl, 4, 2, bt) == 4  # block id 2 >= num_blocks
+
+
+def test_widen_matches_torch_bf16_to_fp32():
+    """oracle.attention.widen (bf16 bit pattern -> fp32) pinned to torch's own bf16 -> fp32
+    conversion on every one of the 65536 bit patterns (NaN payloads compared as NaN), and to
+    closed-form values: 0x3F80 = 1.0, 0xC000 = -2.0, 0x7F80 = +inf, 0x0001 = 2^-133."""
+    import torch
+
+    from oracle.attention import widen
+
+    bits = np.arange(1 << 16, dtype=np.uint32).astype(np.uint16)
+    ours = widen(bits)
+    ref = torch.from_numpy(bits.view(np.int16)).view(torch.bfloat16).float().numpy()
+    nan = np.isnan(ref)
+    assert np.array_equal(np.isnan(ours), nan)
+    assert np.array_equal(ours[~nan].view(np.uint32), ref[~nan].view(np.uint32))
+    w = widen(np.array([0x3F80, 0xC000, 0x7F80, 0x0001], np.uint16))
+    assert w[0] == 1.0 and w[1] == -2.0 and np.isinf(w[2]) and w[2] > 0 and w[3] == np.float32(2.0 ** -133)
+    f = np.array([0.5, -3.25], np.float32)
+    assert np.array_equal(widen(f), f)  # fp32 storage passes through unchanged

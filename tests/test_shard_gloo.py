@@ -22,7 +22,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, mode, q_out):
+def _worker(rank, world, port, mode, layout, q_out):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -31,13 +31,14 @@ def _worker(rank, world, port, mode, q_out):
         from workloads import Workload, generate
 
         w = Workload("shard", ((0, 40), (90, 1), (300, 1), (7, 23), (0, 65), (1000, 1), (33, 1)), 8, 2, 64, 16, "f32")
-        b = generate(w, seed=21, poison=True)
+        b = generate(w, seed=21, poison=True, layout=layout)
         plan = shard.plan_shards(b.cu_seqlens_q, b.seq_lens, w.num_q_heads, w.num_kv_heads, w.head_dim, world, mode)
         lb = shard.local_batch(plan, rank, torch.from_numpy(b.q), torch.from_numpy(b.k_cache),
-                               torch.from_numpy(b.v_cache), b.block_table, b.cu_seqlens_q, b.seq_lens, w.block_size)
+                               torch.from_numpy(b.v_cache), b.block_table, b.cu_seqlens_q, b.seq_lens, w.block_size,
+                               kv_layout=layout)
         local = O.paged_attention(lb.q.numpy(), lb.k_cache.numpy(), lb.v_cache.numpy(), lb.block_table.numpy(),
                                   lb.cu_seqlens_q.numpy(), lb.seq_lens.numpy(), w.scale, lb.num_kv_heads,
-                                  w.block_size)
+                                  w.block_size, layout=layout)
         full = shard.gather_outputs(plan, torch.from_numpy(local), b.cu_seqlens_q, len(lb.q_heads) if mode == "seq"
                                     else len(lb.q_heads))
         if rank == 0:
@@ -48,12 +49,12 @@ def _worker(rank, world, port, mode, q_out):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mode", ["seq", "kvhead"])
-def test_shard_gather_roundtrip_world2(mode):
+@pytest.mark.parametrize("mode,layout", [("seq", "NHD"), ("kvhead", "NHD"), ("seq", "HND"), ("kvhead", "HND")])
+def test_shard_gather_roundtrip_world2(mode, layout):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, mode, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, mode, layout, q)) for r in range(2)]
     for p in procs:
         p.start()
     for p in procs:
