@@ -220,6 +220,11 @@ typedef struct pattn_tuning {
   int32_t items_per_sm;       /* decode: target (segment x KV head x head group) work items per SM (default 16) */
   int32_t min_chunk_tokens;   /* decode: shortest split segment, in keys (default 256) */
   int32_t decode_ctas_per_sm; /* decode: resident K2 CTAs per SM, 1..4 (default 2) */
+  int32_t k2_sm_mbs;          /* mixed batches, two streams: decode streaming rate per SM (MB/s) that K5's
+                                 SM-partition model assumes -- higher leaves more SMs to the prefill kernel
+                                 (default 61000) */
+  int32_t serial;             /* mixed batches: 1 = prefill and decode kernels back to back on one stream
+                                 even when a second stream is given; 0 = concurrent (default) */
 } pattn_tuning_t;           /* 0 in a field = built-in default */
 
 enum {

@@ -79,7 +79,6 @@ namespace {
 constexpr int kHalfM = 128;    // rows per half (one UMMA M)
 constexpr int kM = 2 * kHalfM; // BLOCK_M
 constexpr int kN = 64;         // keys per KV tile
-constexpr int kD = 128;        // head dim
 constexpr int kThreads = 512;  // 16 warps
 // setmaxnreg budgets (16-warp layout): warpgroup 0 (producers, MMA a), warpgroups 1-2
 // (softmax), warpgroup 3 (V producer, scheduler, Q producer, MMA b); 128 (a + d) + 256 s = 65536
@@ -95,12 +94,8 @@ constexpr int kThreads = 512;  // 16 warps
 constexpr int kRegWG0 = PATTN_K1_REG_WG0, kRegSoftmax = PATTN_K1_REG_SOFTMAX, kRegWG3 = PATTN_K1_REG_WG3;
 // setmaxnreg only redistributes the CTA's launch allocation
 static_assert(128 * (kRegWG0 + kRegWG3) + 256 * kRegSoftmax <= 65536, "register budget");
-constexpr uint32_t kQTile = kHalfM * kD * 2;  // 32 KB: one 128-row half of the Q block
-constexpr uint32_t kHalf = kQTile / 2;         // 16 KB: one 64-wide d half of it
-constexpr uint32_t kTile = kN * kD * 2;        // 16 KB: one K or V tile (64 keys)
-constexpr uint32_t kSub16Bytes = 16 * kD * 2;  // 4 KB: one 16-key sub-block of K or V
-// K / V tile layout: sub-block i at i*4K = [8-slot group g][d half h][8 slots][64 d], i.e.
-// 8-key group G = 2i+g at G*2048 + h*1024 (SW128 atoms of 8 rows x 128 B)
+// K / V tile layout: sub-block i (16 keys) = [8-slot group g][d half h][8 slots][64 d], i.e.
+// 8-key group G = 2i+g at G*kGroup + h*1024 (SW128 atoms of 8 rows x 128 B); kGroup = 16*D B.
 #ifndef PATTN_K1_KST
 #define PATTN_K1_KST 3
 #endif
@@ -110,20 +105,30 @@ constexpr uint32_t kSub16Bytes = 16 * kD * 2;  // 4 KB: one 16-key sub-block of 
 constexpr int kKStages = PATTN_K1_KST;
 constexpr int kVStages = PATTN_K1_VST;  // V waits on PV (later than S), so it gets the deeper ring
 constexpr float kRescaleThreshold = 8.0f;  // log2 domain: rescale O only if the max grows by > 2^8
+constexpr uint32_t kBarBlock = 512;        // barriers + the item ring
 
-// shared-memory map (offsets from a 1024-aligned base)
-constexpr uint32_t kOffQ = 0;  // half a: [0, 32K), half b: [32K, 64K)
-constexpr uint32_t kOffK = kOffQ + 2 * kQTile;
-constexpr uint32_t kOffV = kOffK + kKStages * kTile;
-// epilogue staging: per half 16 KB = 4 warps x 32 rows x 128 B (one 64-wide d half at a time),
-// 128B-swizzled as the out TMA map expects
-constexpr uint32_t kStageWarp = 8192;  // both 64-wide d halves staged at once (no read wait in between)
-constexpr uint32_t kStageHalf = 4 * kStageWarp;
-constexpr uint32_t kOffStage = kOffV + kVStages * kTile;
-constexpr uint32_t kOffBar = kOffStage + 2 * kStageHalf;
-constexpr uint32_t kBarBlock = 512;  // barriers + the item ring
-constexpr uint32_t kSmemBytes = kOffBar + kBarBlock + 1024;
-static_assert(kSmemBytes <= 227 * 1024, "shared memory budget");
+// Head-dim dependent sizes and the shared-memory map (offsets from a 1024-aligned base).
+template <int D>
+struct K1Shape {
+  static_assert(D == 64 || D == 128, "head_dim");
+  static constexpr int kHalves = D / 64;                   // 64-wide (128-byte) d halves
+  static constexpr uint32_t kQTile = kHalfM * D * 2;       // one 128-row half of the Q block (32 / 16 KB)
+  static constexpr uint32_t kHalf = kHalfM * 64 * 2;       // 16 KB: one 64-wide d half of a Q half
+  static constexpr uint32_t kTile = kN * D * 2;            // one K or V tile (64 keys: 16 / 8 KB)
+  static constexpr uint32_t kSub16Bytes = 16 * D * 2;      // one 16-key sub-block (4 / 2 KB)
+  static constexpr uint32_t kGroup = 8 * D * 2;            // one 8-key group (2 / 1 KB)
+  static constexpr uint32_t kOffQ = 0;                     // half a, then half b
+  static constexpr uint32_t kOffK = kOffQ + 2 * kQTile;
+  static constexpr uint32_t kOffV = kOffK + kKStages * kTile;
+  // epilogue staging, 128B-swizzled as the out TMA map expects: per warp 32 rows x 128 B per
+  // 64-wide d half, all halves staged at once (no read wait in between)
+  static constexpr uint32_t kStageWarp = 4096 * kHalves;
+  static constexpr uint32_t kStageHalf = 4 * kStageWarp;
+  static constexpr uint32_t kOffStage = kOffV + kVStages * kTile;
+  static constexpr uint32_t kOffBar = kOffStage + 2 * kStageHalf;
+  static constexpr uint32_t kSmemBytes = kOffBar + kBarBlock + 1024;
+  static_assert(kSmemBytes <= 227 * 1024, "shared memory budget");
+};
 
 // TMEM columns
 constexpr uint32_t kTmemS = 0;    // S buffer (half x, tile parity y) at x*128 + y*64 (P aliased on its first 32 cols)
@@ -216,9 +221,14 @@ PATTN_DEVICE Item next_item(Bars& bar, const ItemSlot* ring, uint32_t n, int lan
   return x;
 }
 
+template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
     k1_prefill(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmO,
                const __grid_constant__ KvHeadMaps maps, Params p) {
+  using Sh = K1Shape<D>;
+  constexpr uint32_t kOffQ = Sh::kOffQ, kOffK = Sh::kOffK, kOffV = Sh::kOffV, kOffStage = Sh::kOffStage,
+                     kOffBar = Sh::kOffBar, kQTile = Sh::kQTile, kHalf = Sh::kHalf, kTile = Sh::kTile,
+                     kSub16Bytes = Sh::kSub16Bytes, kStageWarp = Sh::kStageWarp, kGroup = Sh::kGroup;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   Bars& bar = *reinterpret_cast<Bars*>(smem + kOffBar);
@@ -348,11 +358,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int h_lo = warp == 15 ? 1 : 0;
     const int h_hi = h_lo + 1;
     constexpr uint32_t idS = idesc_bf16_f32(kHalfM, kN, 0, 0);   // Q (K-major) x K (K-major)
-    constexpr uint32_t idPV = idesc_bf16_f32(kHalfM, kD, 0, 1);  // P (TMEM, K-major) x V (MN-major)
+    constexpr uint32_t idPV = idesc_bf16_f32(kHalfM, D, 0, 1);  // P (TMEM, K-major) x V (MN-major)
     // smem descriptors: start-address field = addr >> 4, so desc(base + off) = desc(base) + (off >> 4)
     const uint64_t dQ = smem_desc_sw128(sbase + kOffQ, 16, 1024);
-    const uint64_t dK = smem_desc_sw128(sbase + kOffK, 16, 2048);     // 8-key groups 2 KB apart
-    const uint64_t dV = smem_desc_sw128(sbase + kOffV, 1024, 2048);   // d halves 1 KB apart
+    const uint64_t dK = smem_desc_sw128(sbase + kOffK, 16, kGroup);     // 8-key groups kGroup apart
+    const uint64_t dV = smem_desc_sw128(sbase + kOffV, 1024, kGroup);   // d halves 1 KB apart
     const bool leader = elect_one();
     uint32_t ic = 0, kc = 0, vc = 0;
     uint32_t pcnt = 0u;  // PV iterations issued (the same count for every half this warp serves)
@@ -379,7 +389,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               const uint32_t tS = tmem + kTmemS + 128 * h + 64 * (jt & 1);
               const uint64_t dq = dQ + ((h * kQTile) >> 4), dk = dK + ((ks * kTile) >> 4);
 #pragma unroll
-              for (int k = 0; k < kD / 16; ++k) {
+              for (int k = 0; k < D / 16; ++k) {
                 const uint32_t offq = ((k >> 2) * kHalf + (k & 3) * 32) >> 4;
                 const uint32_t offk = ((k >> 2) * 1024 + (k & 3) * 32) >> 4;
                 tc_mma_f16_ss(tS, dq + offq, dk + offk, idS, k > 0 ? 1u : 0u);
@@ -474,11 +484,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (x.ntiles < 0) break;
         if (lane == 0) {
           mbar_wait(&bar.q_empty, (ic & 1u) ^ 1u);
-          mbar_arrive_expect_tx(&bar.q_full, 4u * (uint32_t)(bq_half * G) * 128u);  // 2 halves x 2 d-halves
+          mbar_arrive_expect_tx(&bar.q_full, 2u * Sh::kHalves * (uint32_t)(bq_half * G) * 128u);  // halves x d-halves
           for (int h = 0; h < 2; ++h) {
             const int tok = x.q0 + x.tok0 + h * bq_half;
-            tma_load_4d(smem + kOffQ + h * kQTile, &tmQ, &bar.q_full, 0, 0, x.kvh, tok);
-            tma_load_4d(smem + kOffQ + h * kQTile + kHalf, &tmQ, &bar.q_full, 64, 0, x.kvh, tok);
+#pragma unroll
+            for (int dh = 0; dh < Sh::kHalves; ++dh)
+              tma_load_4d(smem + kOffQ + h * kQTile + dh * kHalf, &tmQ, &bar.q_full, 64 * dh, 0, x.kvh, tok);
           }
         }
         __syncwarp();
@@ -579,7 +590,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           // tcgen05.ld/st are warp-collective (.sync.aligned): rescale when ANY row of the warp needs it
           if (__any_sync(0xffffffffu, alpha != 1.f)) {
 #pragma unroll
-            for (int c0 = 0; c0 < kD; c0 += 32) {
+            for (int c0 = 0; c0 < D; c0 += 32) {
               uint32_t o[32];
               PATTN_TMEM_LD32(tO + c0, o);
               tmem_wait_ld();
@@ -601,9 +612,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t s2 = vc % kVStages;
             mbar_wait(&bar.v_full[s2], (vc / kVStages) & 1u);
             uint8_t* vb = smem + kOffV + s2 * kTile;
-            for (int e = r; e < (z1 - z0) * 16; e += kHalfM) {
-              const int row = z0 + (e >> 4), ch = e & 15;
-              *reinterpret_cast<uint4*>(vb + (row >> 3) * 2048 + (ch >> 3) * 1024 + (row & 7) * 128 + ((ch & 7) << 4)) =
+            constexpr int kCh = D / 8;  // 16-byte chunks per V row
+            for (int e = r; e < (z1 - z0) * kCh; e += kHalfM) {
+              const int row = z0 + e / kCh, ch = e % kCh;
+              *reinterpret_cast<uint4*>(vb + (row >> 3) * kGroup + (ch >> 3) * 1024 + (row & 7) * 128 + ((ch & 7) << 4)) =
                   make_uint4(0, 0, 0, 0);
             }
             fence_proxy_async_smem();
@@ -622,9 +634,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       // this warp's O columns in one go, then O_h is released to the next item's PV_h(0)
       // before the normalisation and the global stores
-      uint32_t o[kD];
+      uint32_t o[D];
 #pragma unroll
-      for (int c0 = 0; c0 < kD; c0 += 32) PATTN_TMEM_LD32(tO + c0, (o + c0));
+      for (int c0 = 0; c0 < D; c0 += 32) PATTN_TMEM_LD32(tO + c0, (o + c0));
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(&bar.o_empty[h]);
@@ -645,7 +657,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t row_off = (uint32_t)(r & 31) * 128;
         const int tok_w = x.q0 + x.tok0 + h * bq_half + (r & ~31) / G;
 #pragma unroll
-        for (int pass = 0; pass < 2; ++pass) {
+        for (int pass = 0; pass < Sh::kHalves; ++pass) {
           uint8_t* stg = stg0 + pass * 4096;
 #pragma unroll
           for (int c = 0; c < 8; ++c) {
@@ -672,7 +684,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         __nv_bfloat16* orow = O + (int64_t)(x.q0 + x.tok0 + tk) * p.o_st_tok +
                               (int64_t)(x.kvh * G + (r % G)) * p.o_st_head;
 #pragma unroll
-        for (int c = 0; c < kD; c += 8) {
+        for (int c = 0; c < D; c += 8) {
           uint4 v;
           uint64_t a = fmul2((uint64_t)o[c + 0] | ((uint64_t)o[c + 1] << 32), inv2);
           v.x = pack_bf16(f32x2_lo(a), f32x2_hi(a));
@@ -701,10 +713,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 bool prefill_supported(const Params& p) {
   if (getenv("PATTN_DISABLE_K1")) return false;
-  // BLOCK_Q = 256/G tokens split into two halves of 128 rows: G must divide 128
   // BLOCK_Q = 2 * floor(128 / G) tokens in two halves of 128 rows (padding rows when G does not
-  // divide 128, e.g. G = 3, 5, 6, 7, 12)
-  return p.D == kD && p.G >= 1 && p.G <= 64 && p.bs % 16 == 0 &&
+  // divide 128, e.g. G = 3, 5, 6, 7, 12); head_dim 64 or 128
+  return (p.D == 64 || p.D == 128) && p.G >= 1 && p.G <= 64 && p.bs % 16 == 0 &&
          p.Hkv <= kMaxKvHeadMaps;
 }
 
@@ -713,16 +724,16 @@ int prefill_block_q(int G) { return 2 * (kHalfM / G); }
 PrefillLaunch plan_prefill(const Params& p, int num_sms) {
   PrefillLaunch pl;
   pl.grid = num_sms;
-  pl.smem = kSmemBytes;
-  (void)p;
+  pl.smem = p.D == 64 ? K1Shape<64>::kSmemBytes : K1Shape<128>::kSmemBytes;
   return pl;
 }
 
 cudaError_t launch_prefill(const Params& p, const PrefillLaunch& pl, const CUtensorMap& tmQ, const CUtensorMap& tmO,
                            const KvHeadMaps& kv, cudaStream_t stream) {
-  cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(k1_prefill), pl.smem);
+  auto kern = p.D == 64 ? k1_prefill<64> : k1_prefill<128>;
+  cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(kern), pl.smem);
   if (e != cudaSuccess) return e;
-  k1_prefill<<<pl.grid, kThreads, pl.smem, stream>>>(tmQ, tmO, kv, p);
+  kern<<<pl.grid, kThreads, pl.smem, stream>>>(tmQ, tmO, kv, p);
   return cudaGetLastError();
 }
 

@@ -123,7 +123,8 @@ TuningTree& tuning_tree() {
 
 bool leaf_ok(const pattn_tuning_t& t) {
   return t.items_per_sm >= 0 && t.items_per_sm <= 4096 && t.min_chunk_tokens >= 0 && t.min_chunk_tokens <= (1 << 24) &&
-         t.decode_ctas_per_sm >= 0 && t.decode_ctas_per_sm <= 4;
+         t.decode_ctas_per_sm >= 0 && t.decode_ctas_per_sm <= 4 && t.k2_sm_mbs >= 0 && t.k2_sm_mbs <= 1000000 &&
+         (t.serial == 0 || t.serial == 1);
 }
 
 double feature_value(const pattn_problem_t* p, int f) {
@@ -139,7 +140,7 @@ double feature_value(const pattn_problem_t* p, int f) {
 
 // Tree leaf for p (all zero when no tree is loaded), then env overrides, then defaults.
 pattn_tuning_t resolve_tuning(const pattn_problem_t* p) {
-  pattn_tuning_t t{0, 0, 0};
+  pattn_tuning_t t{0, 0, 0, 0, 0};
   {
     TuningTree& tt = tuning_tree();
     std::lock_guard<std::mutex> g(tt.mu);
@@ -156,6 +157,9 @@ pattn_tuning_t resolve_tuning(const pattn_problem_t* p) {
   if ((e = getenv("PATTN_ITEMS_PER_SM")) && *e) t.items_per_sm = atoi(e);
   if ((e = getenv("PATTN_MIN_CHUNK_TOKENS")) && *e) t.min_chunk_tokens = atoi(e);
   if ((e = getenv("PATTN_DECODE_CTAS")) && *e) t.decode_ctas_per_sm = atoi(e);
+  if ((e = getenv("PATTN_K2_SM_GBS")) && *e) t.k2_sm_mbs = (int32_t)(atof(e) * 1000.0);
+  if ((e = getenv("PATTN_SERIAL")) && *e) t.serial = atoi(e) ? 1 : 0;
+  if (t.k2_sm_mbs <= 0) t.k2_sm_mbs = 61000;
   if (t.items_per_sm <= 0) t.items_per_sm = 16;
   if (t.min_chunk_tokens <= 0) t.min_chunk_tokens = 256;
   if (t.decode_ctas_per_sm <= 0) t.decode_ctas_per_sm = 2;
@@ -492,8 +496,9 @@ pattn_status_t run(const pattn_problem_t* p, const void* q, const void* k_cache,
   if (st != PATTN_OK) return st;
 
   cudaStream_t s1 = static_cast<cudaStream_t>(stream_v);
-  cudaStream_t s2 = (opts && opts->stream2 && !(p->flags & PATTN_FLAG_SERIAL)) ? static_cast<cudaStream_t>(opts->stream2)
-                                                                               : s1;
+  cudaStream_t s2 = (opts && opts->stream2 && !(p->flags & PATTN_FLAG_SERIAL) && !pl.tuning.serial)
+                        ? static_cast<cudaStream_t>(opts->stream2)
+                        : s1;
   uint8_t* ws = static_cast<uint8_t*>(workspace);
   Params k;
   fill_params(p, pl, &k);
@@ -536,7 +541,7 @@ pattn_status_t run(const pattn_problem_t* p, const void* q, const void* k_cache,
     k.partition = 1;
     k.prefill_ctas_fixed = env_int("PATTN_PREFILL_SMS", 0);
     k.k1_tile_us = env_float("PATTN_K1_TILE_US", 2.8f);
-    k.k2_sm_gbs = env_float("PATTN_K2_SM_GBS", 61.f);
+    k.k2_sm_gbs = (float)pl.tuning.k2_sm_mbs * 1e-3f;
     k.hbm_gbs = env_float("PATTN_HBM_GBS", 6300.f);
   }
 

@@ -11,6 +11,10 @@ Here a configuration is the planner's launch knobs (pattn_tuning_t, include/patt
   items_per_sm        decode work items (segment x KV head x head group) per SM  -> segment count
   min_chunk_tokens    shortest decode segment, in keys
   decode_ctas_per_sm  resident decode CTAs per SM
+  k2_sm_mbs           mixed batches: the per-SM decode rate K5's SM-partition model assumes
+                      (shifts SMs between the concurrent prefill and decode kernels)
+  serial              mixed batches: prefill and decode back to back instead of concurrent
+(0 = the built-in default for any knob).
 and the features are the host-known batch quantities the planner sees (PATTN_FEAT_*):
 num_seqs, num_tokens, max_query_len (1 = decode-only batch), max_seq_len.
 
@@ -27,14 +31,23 @@ import math
 from typing import Dict, Iterable, List, Optional, Sequence, Tuple
 
 FEATURES = ["num_seqs", "num_tokens", "max_query_len", "max_seq_len"]  # order = PATTN_FEAT_*
-KNOBS = ["items_per_sm", "min_chunk_tokens", "decode_ctas_per_sm"]
+KNOBS = ["items_per_sm", "min_chunk_tokens", "decode_ctas_per_sm", "k2_sm_mbs", "serial"]
+
+
+# libpattn's built-in value of each knob (used where a tree leaf or record holds 0)
+DEFAULTS = {"items_per_sm": 16, "min_chunk_tokens": 256, "decode_ctas_per_sm": 2, "k2_sm_mbs": 61000, "serial": 0}
+
+
+def with_defaults(cfg: Dict) -> Dict:
+    """A configuration with 0 ("built-in default") replaced by the default's value."""
+    return {k: int(cfg.get(k, 0)) or DEFAULTS[k] for k in KNOBS}
 
 
 class NoData(ValueError):
     pass
 
 
-def config_key(cfg: Dict) -> Tuple[int, int, int]:
+def config_key(cfg: Dict) -> Tuple[int, ...]:
     return tuple(int(cfg.get(k, 0)) for k in KNOBS)
 
 

@@ -120,6 +120,18 @@ def test_prefill_tensor_core_path(case):
     _check(batch, 0, f"prefill case {case}")
 
 
+@pytest.mark.parametrize("heads,bs,layout", [((8, 8), 16, "NHD"), ((32, 8), 16, "HND"), ((28, 4), 32, "NHD"),
+                                              ((64, 8), 80, "NHD"), ((16, 1), 16, "NHD")])
+def test_prefill_tensor_core_path_head_dim_64(heads, bs, layout):
+    """bf16 head_dim 64 on the tcgen05 prefill kernel (K1 instantiated for D = 64)."""
+    w = Workload("prefill_d64", ((0, 700), (300, 90), (0, 65), (5, 1), (1000, 1)), heads[0], heads[1], 64, bs, "bf16")
+    batch = generate(w, seed=61, dist="peaked", layout=layout, poison=True)
+    db = DeviceBatch(batch)
+    p = P.make_problem(db.q, db.k, heads[1], bs, db.bt, w.num_seqs, None, layout, 700, 1001)
+    assert P.planned_kernels(p) & (1 << P.KERNEL_PREFILL)
+    _check(batch, 0, f"prefill d64 {heads} bs={bs}")
+
+
 def test_chunked_prefill_and_empty_sequences():
     w = Workload("chunked", ((300, 40), (0, 0), (77, 1), (5, 129), (0, 0), (0, 33)), 32, 8, 128, 16, "bf16")
     batch = generate(w, seed=6, dist="peaked")

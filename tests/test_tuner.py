@@ -8,9 +8,9 @@ import pytest
 
 from paper_2511_11581_b200 import tuner
 
-A = {"items_per_sm": 16, "min_chunk_tokens": 256, "decode_ctas_per_sm": 2}
-B = {"items_per_sm": 4, "min_chunk_tokens": 1024, "decode_ctas_per_sm": 3}
-C = {"items_per_sm": 32, "min_chunk_tokens": 64, "decode_ctas_per_sm": 1}
+A = {"items_per_sm": 16, "min_chunk_tokens": 256, "decode_ctas_per_sm": 2, "k2_sm_mbs": 61000, "serial": 0}
+B = {"items_per_sm": 4, "min_chunk_tokens": 1024, "decode_ctas_per_sm": 3, "k2_sm_mbs": 80000, "serial": 0}
+C = {"items_per_sm": 32, "min_chunk_tokens": 64, "decode_ctas_per_sm": 1, "k2_sm_mbs": 45000, "serial": 1}
 
 
 def _rec(label, feats, cfg, mean):
@@ -98,15 +98,16 @@ def test_committed_tree_is_valid_and_installed():
     pattn.load()
     # config 3's shape resolves to the tree's leaf (no env overrides in the test environment)
     p = _problem(pattn, maxq=2048, T=16440)
-    if not any(os.environ.get(k) for k in ("PATTN_ITEMS_PER_SM", "PATTN_MIN_CHUNK_TOKENS", "PATTN_DECODE_CTAS")):
-        assert tuner.planned_tuning(p) == tuner.select(tree, {"num_seqs": 64, "num_tokens": 16440,
-                                                              "max_query_len": 2048, "max_seq_len": 4097})
+    if not any(os.environ.get(k) for k in ("PATTN_ITEMS_PER_SM", "PATTN_MIN_CHUNK_TOKENS", "PATTN_DECODE_CTAS",
+                                           "PATTN_K2_SM_GBS", "PATTN_SERIAL")):
+        assert tuner.planned_tuning(p) == tuner.with_defaults(tuner.select(
+            tree, {"num_seqs": 64, "num_tokens": 16440, "max_query_len": 2048, "max_seq_len": 4097}))
 
 
 def test_libpattn_consults_installed_tree(monkeypatch):
     from paper_2511_11581_b200 import pattn
 
-    for k in ("PATTN_ITEMS_PER_SM", "PATTN_MIN_CHUNK_TOKENS", "PATTN_DECODE_CTAS"):
+    for k in ("PATTN_ITEMS_PER_SM", "PATTN_MIN_CHUNK_TOKENS", "PATTN_DECODE_CTAS", "PATTN_K2_SM_GBS", "PATTN_SERIAL"):
         monkeypatch.delenv(k, raising=False)
     tree = {"feature": "max_query_len", "threshold": 1.5, "lt": B,
             "ge": {"feature": "num_seqs", "threshold": 100, "lt": A, "ge": C}}
@@ -128,6 +129,8 @@ def test_libpattn_consults_installed_tree(monkeypatch):
         bad2 = tuner.flatten({"items_per_sm": 1, "min_chunk_tokens": 1, "decode_ctas_per_sm": 9})
         arr2 = (tuner.TreeNode * 1)(*bad2)
         assert pattn.load().pattn_set_tuning_tree(arr2, 1) == 1
+        bad3 = tuner.flatten(dict(A, serial=2))  # serial is 0 or 1
+        assert pattn.load().pattn_set_tuning_tree((tuner.TreeNode * 1)(*bad3), 1) == 1
         assert tuner.planned_tuning(_problem(pattn)) == B
     finally:
         tuner.install(tuner.default_tree())  # what pattn.load() installs
