@@ -326,38 +326,56 @@ def timed(case, K, W, barrier, with_events=True):
     return ms, kern_ms
 
 
+def fp32_fma_peak_tflops(num_sms, peaks):
+    """SIMT fp32 roof for the generic kernel K4: 128 FP32 lanes x 2 flop (FFMA) per SM per clock at
+    the maximum SM clock (B200_PROFILING.md unit counts; 148 SMs x 128 x 2 x 1.965 GHz = 74.4)."""
+    return num_sms * 128 * 2 * (peaks.get("sm_max") or 1965.0) * 1e6 / 1e12
+
+
 def roofline_of(case, ms, kern_ms, peaks, num_sms, traffic):
     """Per-kernel roofline entries: algorithmic work / the kernel's average event time / the
     FULL measured peak of the GPU (MEASURED_PEAKS.json).  With two streams K1 runs on the P SMs
-    K5 gave it; the fraction of that share's roof is reported separately (`frac_of_sm_share`)."""
+    K5 gave it; the fraction of that share's roof is reported separately (`frac_of_sm_share`).
+    `ideal_ms` = work / peak orders the kernels: the one with the largest is the step's
+    dominant roof (concurrent kernels can share the same event span)."""
     work = kernel_work(case.w)
     rl = {}
     pre_name = "prefill" if "prefill" in kern_ms else ("generic" if "generic" in kern_ms else None)
     if pre_name and work["prefill_flops"] > 0:
         t = kern_ms[pre_name] * 1e-3
         a = work["prefill_flops"] / t / 1e12
-        pk = peaks["bf16"]
-        e = {"bound": "tensor", "achieved": a, "peak": pk, "unit": "TFLOP/s", "frac": a / pk,
+        if pre_name == "prefill":
+            bound, pk = "tensor", peaks["bf16"]
+        else:  # SIMT fallback / fp32 path
+            bound, pk = "alu", fp32_fma_peak_tflops(num_sms, peaks)
+        e = {"bound": bound, "achieved": a, "peak": pk, "unit": "TFLOP/s", "frac": a / pk,
              "traffic": traffic.get(pre_name), "kernel": pre_name, "kernel_ms": kern_ms[pre_name],
-             "share_of_step": kern_ms[pre_name] / ms,
+             "share_of_step": kern_ms[pre_name] / ms, "ideal_ms": work["prefill_flops"] / (pk * 1e12) * 1e3,
              "algorithmic_unit": "4*D*Hq*(ctx_b+i+1) flop per prefill query token (visible pairs only)"}
         if pre_name == "prefill" and case.streams == 2 and "decode" in kern_ms:
             sms = case.prefill_sms()
             e["prefill_sms"] = sms
             e["frac_of_sm_share"] = a / (pk * sms / num_sms)
         rl["prefill"] = e
-    if "decode" in kern_ms and work["decode_bytes"] > 0:
-        t = kern_ms["decode"] * 1e-3
+    dec_name = "decode" if "decode" in kern_ms else ("generic" if "generic" in kern_ms else None)
+    if dec_name and work["decode_bytes"] > 0:
+        t = kern_ms[dec_name] * 1e-3
         a = work["decode_bytes"] / t / 1e9
         rl["decode"] = {"bound": "hbm", "achieved": a, "peak": peaks["hbm"], "unit": "GB/s", "frac": a / peaks["hbm"],
-                        "traffic": traffic.get("decode"), "kernel": "decode", "kernel_ms": kern_ms["decode"],
-                        "share_of_step": kern_ms["decode"] / ms,
-                        "algorithmic_unit": "L_b*Hkv*2*D*2 B of K+V + 2*Hq*D*2 B of q/out per decode sequence"}
+                        "traffic": traffic.get(dec_name), "kernel": dec_name, "kernel_ms": kern_ms[dec_name],
+                        "share_of_step": kern_ms[dec_name] / ms,
+                        "ideal_ms": work["decode_bytes"] / (peaks["hbm"] * 1e9) * 1e3,
+                        "algorithmic_unit": "L_b*Hkv*2*D*esz B of K+V + 2*Hq*D*esz B of q/out per decode sequence"}
     if "baseline" in kern_ms:  # the paper's App. A kernel (--flags 16): SIMT, reported by time only
         rl["baseline"] = {"bound": "alu", "achieved": work["total_flops"] / (kern_ms["baseline"] * 1e-3) / 1e12,
                           "peak": None, "unit": "TFLOP/s", "frac": None, "traffic": None, "kernel": "baseline",
-                          "kernel_ms": kern_ms["baseline"], "share_of_step": kern_ms["baseline"] / ms}
+                          "kernel_ms": kern_ms["baseline"], "share_of_step": kern_ms["baseline"] / ms,
+                          "ideal_ms": 0.0}
     return rl
+
+
+def dominant_roof(rl):
+    return max(rl.values(), key=lambda r: (r["ideal_ms"], r["kernel_ms"])) if rl else None
 
 
 def sub_result(name, w, dev, pattn, streams, K, W, peaks, num_sms, l2, barrier, seed):
@@ -367,7 +385,7 @@ def sub_result(name, w, dev, pattn, streams, K, W, peaks, num_sms, l2, barrier, 
     case = Case(w, seed, dev, pattn, streams, 0, l2)
     ms, kern_ms = timed(case, K, W, barrier)
     rl = roofline_of(case, ms, kern_ms, peaks, num_sms, load_traffic(name))
-    dom = max(rl.values(), key=lambda r: r["kernel_ms"]) if rl else None
+    dom = dominant_roof(rl)
     r = {"workload": name, "streams": streams, "ms_per_step": ms, "value": w.num_tokens / (ms * 1e-3),
          "unit": "tokens/s", "kernel_ms": kern_ms, "replicas": case.replicas,
          "l2": "inputs %.2f GB %s" % (case.ws_bytes / 1e9, "> 2x L2, no flush" if case.replicas == 1 else
@@ -425,7 +443,10 @@ def strong_scaling_c5(args, dev, pattn, world, rank, barrier, l2):
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_max = float(t.item())
-        gathered = shard.gather_outputs(plan, case.out, cu_h, w.num_q_heads)
+        if dist.get_backend() == "gloo":  # test-only multi-rank runs on one GPU: gather on the host
+            gathered = shard.gather_outputs(plan, case.out.cpu(), cu_h, w.num_q_heads).to(dev)
+        else:  # NCCL over NVLink
+            gathered = shard.gather_outputs(plan, case.out, cu_h, w.num_q_heads)
         entry = {"ms_per_step": ms_max, "value": w.num_tokens / (ms_max * 1e-3), "unit": "tokens/s",
                  "local_seqs": int(lw.num_seqs), "local_heads": f"{lw.num_q_heads}q/{lw.num_kv_heads}kv",
                  "replicas": case.replicas}
@@ -490,7 +511,7 @@ def main():
         if world > 1:
             dist.barrier()
 
-    w_global = CONFIGS[args.workload] if args.workload in CONFIGS else ATTRIBUTION[args.workload]
+    w_global = CONFIGS[args.workload] if args.workload in CONFIGS else ATTRIBUTION[args.workload]  # + envelope shapes
     shard_world = args.sim_world if args.sim_world else world
     shard_rank = args.sim_rank if args.sim_world else rank
     w = local_workload(w_global, args.shard, shard_world, shard_rank)
@@ -601,7 +622,7 @@ def main():
         del q_h, outs_h, hws
 
     rl = roofline_of(case, ms, kern_ms, peaks, num_sms, load_traffic(args.workload))
-    dominant = max(rl.values(), key=lambda r: r["kernel_ms"]) if rl else None
+    dominant = dominant_roof(rl)
     kv_gb = kc.numel() * 2 * kc.element_size() / 1e9
     work = kernel_work(w)
     del case, inp, q, kc

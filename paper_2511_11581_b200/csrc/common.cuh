@@ -176,6 +176,14 @@ PATTN_DEVICE int sm_id() {
   return (int)id;
 }
 
+// Two-stream SM partition: does SM `smid` belong to the prefill kernel when it owns P of the N
+// SMs?  The P SMs are spread evenly over the %smid range (a Bresenham selection), so both
+// kernels get SMs of every GPC and of both dies instead of one contiguous block of IDs.
+PATTN_DEVICE bool partition_prefill_sm(int smid, int P, int N) {
+  if (smid >= N) return false;
+  return ((smid + 1) * P) / N > (smid * P) / N;
+}
+
 // Non-blocking: has the phase with this parity completed?
 PATTN_DEVICE bool mbar_test(uint64_t* bar, uint32_t parity) {
   uint32_t ok;

@@ -236,14 +236,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t sbase = smem_u32(smem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   PATTN_CTA_BEGIN(k1);
-  // two-stream SM partition (K5's choice): K1 works on the SMs with %smid < P; a CTA placed on
-  // another SM leaves it to the decode kernel at once.  Keyed on the physical SM (not blockIdx),
+  // two-stream SM partition (K5's choice): K1 works on P SMs spread over the %smid range; a CTA
+  // placed on another SM leaves it to the decode kernel at once.  Keyed on the physical SM (not blockIdx),
   // so it holds whichever kernel the hardware (or a replayed CUDA graph, whose two branches
   // start in either order) launches first.  CTA 0 always works (progress guarantee).
 #ifdef PATTN_PARTITION_BLOCKIDX  // A/B: the round-1 rule (CTA index, launch-order dependent)
   if (p.partition && (int)blockIdx.x >= p.hdr[kHdrPrefillCtas]) return;
 #else
-  if (p.partition && blockIdx.x != 0 && sm_id() >= p.hdr[kHdrPrefillCtas]) return;
+  if (p.partition && blockIdx.x != 0 && !partition_prefill_sm(sm_id(), p.hdr[kHdrPrefillCtas], p.num_sms)) return;
 #endif
 #ifdef PATTN_TRACE
   const int trace_role = warp == 15 ? -1 : warp == 1 ? 0 : warp == 0 ? 3 : warp == 3 ? 4 : warp == 4 ? 1 : 2;

@@ -111,14 +111,14 @@ __global__ void __launch_bounds__((NCW + kNP) * 32, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   PATTN_CTA_BEGIN(k2);
   if (p.partition && !PATTN_PARTITION_BLOCKIDX_ON) {
-    // two-stream SM partition: the SMs with %smid < P belong to the prefill kernel K1 while it
+    // two-stream SM partition: K5's P SMs belong to the prefill kernel K1 while it
     // still has Q blocks to claim -- a decode CTA placed there first (graph replays launch the
     // two branches in either order) leaves at once.  CTA 0 always works (progress guarantee).
     __shared__ int s_leave;
     if (threadIdx.x == 0) {
       const int pre_left = *reinterpret_cast<volatile int*>(p.hdr + kHdrPrefillCounter) <
                            p.hdr[kHdrTotalQBlocks] * p.Hkv;
-      s_leave = blockIdx.x != 0 && sm_id() < p.hdr[kHdrPrefillCtas] && pre_left;
+      s_leave = blockIdx.x != 0 && partition_prefill_sm(sm_id(), p.hdr[kHdrPrefillCtas], p.num_sms) && pre_left;
     }
     __syncthreads();
     if (s_leave) return;

@@ -99,18 +99,43 @@ __global__ void __launch_bounds__(kWarps * 32) k4_generic(Params p) {
 
     for (int t0 = kv_begin; t0 < kv_end; t0 += kTileKeys) {
       __syncthreads();
-      for (int idx = threadIdx.x; idx < kTileKeys * D; idx += kWarps * 32) {
-        int jj = idx / D, d = idx - jj * D;
-        int t = t0 + jj;
-        float kx = 0.f, vx = 0.f;
-        if (t < kv_end) {  // never touch slots past the visible range (may hold NaN, reading R13)
-          int64_t off = (int64_t)bt[t / p.bs] * p.kv_st_blk + (int64_t)(t % p.bs) * p.kv_st_tok +
-                        (int64_t)kvh * p.kv_st_head + d;
-          kx = to_f32(K[off]);
-          vx = to_f32(V[off]);
+      if (p.kv_vec16) {
+        // 16-byte loads (8 bf16 / 4 fp32 per thread and operand): the tile's K and V rows are
+        // contiguous head_dim vectors, so a warp reads whole 128-byte lines
+        constexpr int kVec = 16 / (int)sizeof(T), kChunks = D / kVec;
+#pragma unroll 2
+        for (int idx = threadIdx.x; idx < kTileKeys * kChunks; idx += kWarps * 32) {
+          const int jj = idx / kChunks, d = (idx - jj * kChunks) * kVec;
+          const int t = t0 + jj;
+          uint4 kr = make_uint4(0, 0, 0, 0), vr = make_uint4(0, 0, 0, 0);
+          if (t < kv_end) {  // never touch slots past the visible range (may hold NaN, reading R13)
+            const int64_t off = (int64_t)bt[t / p.bs] * p.kv_st_blk + (int64_t)(t % p.bs) * p.kv_st_tok +
+                                (int64_t)kvh * p.kv_st_head + d;
+            kr = __ldg(reinterpret_cast<const uint4*>(K + off));
+            vr = __ldg(reinterpret_cast<const uint4*>(V + off));
+          }
+          const T* ke = reinterpret_cast<const T*>(&kr);
+          const T* ve = reinterpret_cast<const T*>(&vr);
+#pragma unroll
+          for (int e = 0; e < kVec; ++e) {
+            sK[jj * (D + 1) + d + e] = to_f32(ke[e]);
+            sV[jj * D + d + e] = to_f32(ve[e]);
+          }
         }
-        sK[jj * (D + 1) + d] = kx;
-        sV[jj * D + d] = vx;
+      } else {
+        for (int idx = threadIdx.x; idx < kTileKeys * D; idx += kWarps * 32) {
+          int jj = idx / D, d = idx - jj * D;
+          int t = t0 + jj;
+          float kx = 0.f, vx = 0.f;
+          if (t < kv_end) {  // never touch slots past the visible range (may hold NaN, reading R13)
+            int64_t off = (int64_t)bt[t / p.bs] * p.kv_st_blk + (int64_t)(t % p.bs) * p.kv_st_tok +
+                          (int64_t)kvh * p.kv_st_head + d;
+            kx = to_f32(K[off]);
+            vx = to_f32(V[off]);
+          }
+          sK[jj * (D + 1) + d] = kx;
+          sV[jj * D + d] = vx;
+        }
       }
       __syncthreads();
 

@@ -37,6 +37,7 @@ struct Params {
   int32_t max_chunks;     // capacity of the partial buffers, in chunks
   int32_t decode_split;   // 1: q_b == 1 sequences are split-KV decode units (segments, K3 merge)
   int32_t k4_decodes;     // 1: those decode segments run on K4 (fp32 / block sizes K2 cannot fetch)
+  int32_t kv_vec16;       // 1: K/V rows start 16-byte aligned (K4 loads them as 16-byte vectors)
   int32_t split_mode;     // 0 planner, 1 no split, 2 force split
   int32_t target_items;   // decode: desired number of (chunk, kv head, head group) items
   int32_t min_chunk_blocks;

@@ -170,6 +170,7 @@ pattn_tuning_t resolve_tuning(const pattn_problem_t* p) {
 struct Plan {
   bool use_k1 = false, use_k2 = false, use_k4 = false, use_k7 = false;
   bool k4_decodes = false;  // decode segments on K4 (when K2 cannot take them)
+  bool kv_vec16 = false;    // K/V rows 16-byte aligned (K4 vector loads)
   int block_q = 1, HG = 1, rpw = 8;
   int target_items = 0, min_chunk = 1, split_mode = 0, max_chunks = 0;
   int num_sms = 148;
@@ -215,6 +216,7 @@ void fill_params(const pattn_problem_t* p, const Plan& pl, Params* k) {
   k->max_chunks = pl.max_chunks;
   k->decode_split = (pl.use_k2 || pl.k4_decodes) ? 1 : 0;
   k->k4_decodes = pl.k4_decodes ? 1 : 0;
+  k->kv_vec16 = pl.kv_vec16 ? 1 : 0;
   k->split_mode = pl.split_mode;
   k->target_items = pl.target_items;
   k->min_chunk_blocks = pl.min_chunk;
@@ -279,6 +281,9 @@ pattn_status_t make_plan(const pattn_problem_t* p, const void* q, const void* kc
   const bool o_vec = (p->o_stride_tok * esz) % 16 == 0 && (p->o_stride_head * esz) % 16 == 0 &&
                      (out == nullptr || aligned16(out));
   pl->k4_decodes = !pl->use_k2 && !pl->use_k7 && o_vec;
+  pl->kv_vec16 = (p->kv_stride_blk * esz) % 16 == 0 && (p->kv_stride_tok * esz) % 16 == 0 &&
+                 (p->kv_stride_head * esz) % 16 == 0 && (D * esz) % 16 == 0 && (kc == nullptr || aligned16(kc)) &&
+                 (vc == nullptr || aligned16(vc));
   if (pl->k4_decodes) pl->use_k4 = true;
   const int bm = pl->block_q * G;
   pl->rpw = bm <= 32 ? 8 : 16;

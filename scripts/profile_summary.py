@@ -24,6 +24,11 @@ METRICS = [
     "SM_A.TriageCompute.sm__inst_executed_pipe_xu_realtime.avg.pct_of_peak_sustained_elapsed",
     "sm__inst_executed_pipe_tc.avg.pct_of_peak_sustained_active",
     "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+    "sm__ops_path_tensor_op_utchmma_src_bf16_dst_fp32_sparsity_off.avg.pct_of_peak_sustained_elapsed",
+    "sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_elapsed",
+    "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_elapsed",
+    "sm__issue_active.avg.pct_of_peak_sustained_elapsed",
     "smsp__issue_active.avg.pct_of_peak_sustained_active",
     "sm__warps_active.avg.pct_of_peak_sustained_active",
     "launch__registers_per_thread",
@@ -50,7 +55,7 @@ def main(rnd):
     traffic = {}
     lines = []
     for f in sorted(os.listdir(src)):
-        if f.startswith("ncu_c") and f.endswith(".csv"):
+        if f.startswith("ncu_") and f.endswith(".csv") and f != "ncu_k1_tensor.csv":
             wl = f[4:-4]
             shutil.copy(os.path.join(src, f), os.path.join(dst, f"launches_{wl}.csv"))
             agg = load(os.path.join(src, f))
@@ -66,7 +71,7 @@ def main(rnd):
                 name = {"k1_prefill": "prefill", "k2_decode": "decode", "k3_reduce": "reduce",
                         "k4_generic": "generic", "k5_metadata": "metadata"}.get(k, k)
                 traffic.setdefault(wl, {})[name] = (sum(rd) + sum(wr)) / n
-    for rep in ("k1_c3_full", "k2_c2_full", "k2_c4_full", "k3_c4_full", "k6_c3_full"):
+    for rep in ("k1_c3_full", "k1_c3p_full", "k2_c2_full", "k2_c4_full", "k2_sm36", "k3_c4_full", "k6_c3_full"):
         path = os.path.join(src, rep + ".ncu-rep")
         if os.path.exists(path):
             shutil.copy(path, os.path.join(dst, rep + ".ncu-rep"))
@@ -74,7 +79,7 @@ def main(rnd):
             for k, (v, u) in raw_metrics(path).items():
                 lines.append(f"  {k} = {v} {u}")
     for f in sorted(os.listdir(src)):
-        if f.startswith("bench_c") and f.endswith(".json"):
+        if f.startswith("bench_") and f.endswith(".json"):
             shutil.copy(os.path.join(src, f), os.path.join(dst, f))
     open(os.path.join(dst, "summary.txt"), "w").write("\n".join(lines) + "\n")
     tpath = os.path.join(ROOT, "profiles", "traffic.json")

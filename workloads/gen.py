@@ -126,6 +126,13 @@ CONFIGS: Dict[str, Workload] = {
 ATTRIBUTION: Dict[str, Workload] = {
     "c3p_prefill_part": CONFIGS["c3_mixed8b"].with_seqs([(0, 2048)] * 8, name="c3p_prefill_part"),
     "c3d_decode_part": CONFIGS["c3_mixed8b"].with_seqs([(4096, 1)] * 56, name="c3d_decode_part"),
+    # shapes outside the BASELINE configs that exercise the widened kernel envelope (bench lines)
+    # GQA 7:1 (28 query / 4 KV heads, e.g. Qwen2-7B): the tcgen05 prefill with padding rows
+    "x_g7_mixed": Workload("x_g7_mixed", tuple([(0, 2048)] * 8 + [(4096, 1)] * 56), 28, 4, 128, 16, "bf16"),
+    # head_dim 64 (32 / 8 heads): the D = 64 instantiation of the tcgen05 prefill kernel
+    "x_d64_mixed": Workload("x_d64_mixed", tuple([(0, 2048)] * 8 + [(4096, 1)] * 56), 32, 8, 64, 16, "bf16"),
+    # block size 7 (not a multiple of 16): long decodes split on the SIMT kernel, merged by K3
+    "x_bs7_decode32k": Workload("x_bs7_decode32k", tuple((32768, 1) for _ in range(8)), 32, 8, 128, 7, "bf16"),
 }
 
 
