@@ -560,3 +560,45 @@ def test_bf16_error_stays_at_the_rounding_level(dist, heads, D):
     assert (err <= bound).all(), f"{dist} {heads} D{D}: max err/bound {float((err / bound).max()):.2f}"
     rms = float(np.sqrt((err ** 2).mean()))
     assert rms <= 2.0 ** -9 * vmax, f"{dist} {heads} D{D}: rms err {rms:.2e}"
+
+
+def test_two_stream_partition_follows_the_mix():
+    """K5's SM partition (workspace header word kHdrPrefillCtas, the K1 share P) on batches of
+    the same heads with a growing prefill share: P stays inside [1, #SMs - 1], grows with the
+    prefill work, and the prefill-only / decode-heavy extremes land near the ends."""
+    from paper_2511_11581_b200 import pattn
+
+    num_sms = torch.cuda.get_device_properties(0).multi_processor_count
+    shares = []
+    for npre in (1, 2, 4, 8, 16):
+        w = Workload(f"part{npre}", tuple([(0, 1024)] * npre + [(4096, 1)] * 48), 32, 8, 128, 16, "bf16")
+        batch = generate(w, seed=npre, poison=False)
+        db = DeviceBatch(batch)
+        ws = torch.empty(1 << 24, dtype=torch.uint8, device="cuda")
+        db.run(stream2=torch.cuda.Stream(), workspace=ws)
+        P = pattn.workspace_prefill_sms(ws)
+        assert 1 <= P <= num_sms - 1, (npre, P)
+        shares.append(P)
+    assert shares == sorted(shares), shares  # more prefill work -> more SMs for K1
+    assert shares[-1] > shares[0]
+
+
+# ---------------------------------------------------------------- shape fuzz
+FUZZ_HEADS = [(32, 8), (64, 8), (28, 4), (48, 8), (16, 1), (8, 8), (40, 8), (12, 2), (96, 8), (24, 3)]
+
+
+@pytest.mark.parametrize("i", range(24))
+def test_shape_fuzz(i):
+    """Seeded random shapes across every routing decision: heads (G = 1..12), head_dim 64/128,
+    block sizes that K1/K2 take (16·k) and that only K4 takes (5, 7, 24), NHD/HND, bf16/fp32,
+    ragged mixed batches with chunked prefills and long decodes, poisoned unused slots."""
+    rng = np.random.default_rng(9000 + i)
+    heads = FUZZ_HEADS[int(rng.integers(len(FUZZ_HEADS)))]
+    D = int(rng.choice([64, 128]))
+    bs = int(rng.choice([16, 32, 48, 80, 128, 5, 7, 24]))
+    dt = "f32" if rng.random() < 0.2 else "bf16"
+    layout = "HND" if rng.random() < 0.4 else "NHD"
+    w = random_workload(rng, heads, D, bs, dt, max_seqs=7, max_len=int(rng.choice([300, 1200, 2500])),
+                        decode_share=float(rng.uniform(0.2, 0.8)))
+    batch = generate(w, seed=i, dist="peaked", layout=layout, poison=True)
+    _check(batch, 0, f"fuzz {i}: heads {heads} D{D} bs{bs} {dt} {layout} {w.seqs}")
