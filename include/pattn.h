@@ -35,6 +35,15 @@
  *   - Thread safety: concurrent calls are safe when they use distinct
  *     workspaces.  The library caches only immutable per-device data.
  *   - q_b = 0 sequences are legal (padding) and produce no rows.
+ *   - Host hints (pattn_problem_t.max_query_len / max_seq_len) must be upper bounds.  A
+ *     max_query_len below the true maximum can drop the Q-block kernel from the plan; the
+ *     metadata kernel flags it in the workspace, and with the environment variable
+ *     PATTN_DEBUG_SYNC=1 every call synchronises its stream and returns
+ *     PATTN_ERR_INVALID_SEQUENCE in that case (debugging aid; not for the hot path, and
+ *     skipped while the stream is being captured into a CUDA graph).
+ *   - Environment overrides of the planner (sweeps and A/B only): PATTN_ITEMS_PER_SM,
+ *     PATTN_MIN_CHUNK_TOKENS, PATTN_DECODE_CTAS, PATTN_K2_SM_GBS, PATTN_SERIAL (see
+ *     pattn_tuning_t), PATTN_PREFILL_SMS (fixed two-stream split), PATTN_DISABLE_K1.
  */
 #ifndef PATTN_H_
 #define PATTN_H_

@@ -587,7 +587,7 @@ def test_two_stream_partition_follows_the_mix():
 FUZZ_HEADS = [(32, 8), (64, 8), (28, 4), (48, 8), (16, 1), (8, 8), (40, 8), (12, 2), (96, 8), (24, 3)]
 
 
-@pytest.mark.parametrize("i", range(24))
+@pytest.mark.parametrize("i", range(48))
 def test_shape_fuzz(i):
     """Seeded random shapes across every routing decision: heads (G = 1..12), head_dim 64/128,
     block sizes that K1/K2 take (16·k) and that only K4 takes (5, 7, 24), NHD/HND, bf16/fp32,
