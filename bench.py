@@ -298,32 +298,48 @@ class Case:
 
 def timed(case, K, W, barrier, with_events=True):
     """W untimed calls, then K calls between CUDA events on the launching stream (barrier +
-    synchronize on both sides); per-kernel averages from the library's event hooks."""
+    synchronize on both sides): the step time.  With `with_events`, a second timed region of K
+    calls follows in which the library records CUDA events around every kernel
+    (pattn_exec_opts_t.events) -- the per-kernel averages for the roofline.  The two are
+    separate because those per-kernel event records are not free: they add ~2 us between
+    kernels (config 2: 177 us per call plain vs 193 us instrumented), so the step time is
+    measured without them.  Returns (ms_per_step, kernel_ms, instrumented_ms_per_step)."""
     import torch
 
     pattn = case.pattn
     for i in range(max(3, W)):
         case.step(i)
     torch.cuda.synchronize()
-    kev = pattn.make_events(K) if with_events else None
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    barrier()
-    torch.cuda.synchronize()
-    t0.record(case.stream)
-    for i in range(K):
-        case.step(i, events=kev[i] if kev else None)
-    t1.record(case.stream)
-    torch.cuda.synchronize()
-    barrier()
-    ms = t0.elapsed_time(t1) / K
-    kern_ms = {}
-    if kev:
+
+    def region(kev):
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        torch.cuda.synchronize()
+        t0.record(case.stream)
+        for i in range(K):
+            case.step(i, events=kev[i] if kev else None)
+        t1.record(case.stream)
+        torch.cuda.synchronize()
+        barrier()
+        return t0.elapsed_time(t1) / K
+
+    ms = region(None)
+    kern_ms, ms_instr = {}, None
+    if with_events:
+        kev = pattn.make_events(K)
+        # the two regions are separate measurements: let the clocks recover from the first
+        # (a long tensor-core burst can drop the SM clock) and warm up again before the second
+        time.sleep(0.5)
+        for i in range(3):
+            case.step(i)
+        torch.cuda.synchronize()
+        ms_instr = region(kev)
         kmask = pattn.planned_kernels(case.prob)
         for k in range(pattn.KERNEL_COUNT):
             if kmask & (1 << k):
                 kern_ms[pattn.KERNEL_NAMES[k]] = sum(kev[i][2 * k].elapsed_time(kev[i][2 * k + 1])
                                                      for i in range(K)) / K
-    return ms, kern_ms
+    return ms, kern_ms, ms_instr
 
 
 def fp32_fma_peak_tflops(num_sms, peaks):
@@ -383,11 +399,11 @@ def sub_result(name, w, dev, pattn, streams, K, W, peaks, num_sms, l2, barrier, 
     import torch
 
     case = Case(w, seed, dev, pattn, streams, 0, l2)
-    ms, kern_ms = timed(case, K, W, barrier)
-    rl = roofline_of(case, ms, kern_ms, peaks, num_sms, load_traffic(name))
+    ms, kern_ms, ms_instr = timed(case, K, W, barrier)
+    rl = roofline_of(case, ms_instr, kern_ms, peaks, num_sms, load_traffic(name))
     dom = dominant_roof(rl)
     r = {"workload": name, "streams": streams, "ms_per_step": ms, "value": w.num_tokens / (ms * 1e-3),
-         "unit": "tokens/s", "kernel_ms": kern_ms, "replicas": case.replicas,
+         "unit": "tokens/s", "kernel_ms": kern_ms, "instrumented_ms_per_step": ms_instr, "replicas": case.replicas,
          "l2": "inputs %.2f GB %s" % (case.ws_bytes / 1e9, "> 2x L2, no flush" if case.replicas == 1 else
                                       f"< 2x L2: {case.replicas} rotated replicas"),
          "roofline": ({k: dom[k] for k in ("bound", "achieved", "peak", "unit", "frac", "traffic", "kernel")}
@@ -419,7 +435,7 @@ def strong_scaling_c5(args, dev, pattn, world, rank, barrier, l2):
     ref = None
     if rank == 0:
         full = Case(w, 0, dev, pattn, 2, 0, l2, inp=g)
-        ms1, _ = timed(full, K, args.warmup, lambda: None, with_events=False)
+        ms1, _, _ = timed(full, K, args.warmup, lambda: None, with_events=False)
         ref = full.out.clone()
         res["one_gpu_ms"] = ms1
         del full
@@ -439,7 +455,7 @@ def strong_scaling_c5(args, dev, pattn, world, rank, barrier, l2):
         linp = dict(q=lb.q, k_cache=lb.k_cache, v_cache=lb.v_cache, block_table=lb.block_table,
                     cu_seqlens_q=lb.cu_seqlens_q, seq_lens=lb.seq_lens)
         case = Case(lw, 0, dev, pattn, 2, 0, l2, inp=linp)
-        ms, _ = timed(case, K, args.warmup, barrier, with_events=False)
+        ms, _, _ = timed(case, K, args.warmup, barrier, with_events=False)
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_max = float(t.item())
@@ -523,7 +539,7 @@ def main():
 
     sampler = ClockSampler(local)
     with sampler:
-        ms, kern_ms = timed(case, K, args.warmup, barrier)
+        ms, kern_ms, ms_instr = timed(case, K, args.warmup, barrier)
 
     if args.shard == "none":
         tokens_all = w.num_tokens * world  # weak scaling: every rank runs the full workload
@@ -621,7 +637,7 @@ def main():
                "d2h_bytes_per_step": d2h, "ms_per_step": float(ems.item()), "requests_in_flight": 2}
         del q_h, outs_h, hws
 
-    rl = roofline_of(case, ms, kern_ms, peaks, num_sms, load_traffic(args.workload))
+    rl = roofline_of(case, ms_instr, kern_ms, peaks, num_sms, load_traffic(args.workload))
     dominant = dominant_roof(rl)
     kv_gb = kc.numel() * 2 * kc.element_size() / 1e9
     work = kernel_work(w)
@@ -696,12 +712,14 @@ def main():
                      if dominant else None),
         "roofline_kernels": rl,
         "kernel_ms": kern_ms,
+        "instrumented_ms_per_step": ms_instr,
         "clocks": sampler.summary(),
         "e2e": e2e,
         "cuda_graph": graph,
         "gpu_launches": launches_per_step * K,
         "cpu_baseline": cpu,
         "sub_results": subs,
+        "gpu_launches_note": "gpu_launches counts the K timed calls of the step-time region",
         "algorithmic": {"prefill_tflop_per_step": work["prefill_flops"] / 1e12,
                         "decode_gb_per_step": work["decode_bytes"] / 1e9,
                         "step_tflops": work["total_flops"] / (ms * 1e-3) / 1e12,
