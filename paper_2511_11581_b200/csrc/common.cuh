@@ -190,6 +190,14 @@ PATTN_DEVICE bool partition_prefill_sm(int smid, int P, int N) {
 #endif
 }
 
+// Programmatic dependent launch (PDL).  A kernel launched with programmatic stream
+// serialization may start while its predecessor in the stream still runs; pdl_wait() blocks
+// until the predecessor grid has completed and its memory is visible, so it must precede every
+// read of the predecessor's results (a no-op for kernels launched without the attribute).
+// pdl_trigger() lets this grid's own dependents launch early (once every CTA triggered/exited).
+PATTN_DEVICE void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+PATTN_DEVICE void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // Non-blocking: has the phase with this parity completed?
 PATTN_DEVICE bool mbar_test(uint64_t* bar, uint32_t parity) {
   uint32_t ok;

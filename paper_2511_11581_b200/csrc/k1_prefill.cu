@@ -236,6 +236,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t sbase = smem_u32(smem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   PATTN_CTA_BEGIN(k1);
+  pdl_wait();  // K5's metadata (and the SM partition) is complete and visible
   // two-stream SM partition (K5's choice): K1 works on P SMs spread over the %smid range; a CTA
   // placed on another SM leaves it to the decode kernel at once.  Keyed on the physical SM (not blockIdx),
   // so it holds whichever kernel the hardware (or a replayed CUDA graph, whose two branches
@@ -733,8 +734,7 @@ cudaError_t launch_prefill(const Params& p, const PrefillLaunch& pl, const CUten
   auto kern = p.D == 64 ? k1_prefill<64> : k1_prefill<128>;
   cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(kern), pl.smem);
   if (e != cudaSuccess) return e;
-  kern<<<pl.grid, kThreads, pl.smem, stream>>>(tmQ, tmO, kv, p);
-  return cudaGetLastError();
+  return launch_pdl(kern, dim3(pl.grid), dim3(kThreads), pl.smem, stream, tmQ, tmO, kv, p);
 }
 
 }  // namespace pattn

@@ -110,6 +110,7 @@ __global__ void __launch_bounds__((NCW + kNP) * 32, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   PATTN_CTA_BEGIN(k2);
+  pdl_wait();  // K5's metadata (or, serial, the previous kernel's work) is complete and visible
   if (p.partition && !PATTN_PARTITION_BLOCKIDX_ON) {
     // two-stream SM partition: K5's P SMs belong to the prefill kernel K1 while it
     // still has Q blocks to claim -- a decode CTA placed there first (graph replays launch the
@@ -167,7 +168,10 @@ __global__ void __launch_bounds__((NCW + kNP) * 32, 1)
         }
       }
       it = __shfl_sync(0xffffffffu, it, 0);
-      if (it >= n_items) break;
+      if (it >= n_items) {
+        if (pw == 0 && lane == 0) pdl_trigger();  // no more items here: K3 may be scheduled
+        break;
+      }
       const Item x = decode_item(p, it);
       const int32_t* bt = p.block_table + (int64_t)x.b * p.bt_stride;
       for (int j0 = x.sb0; j0 < x.sb1; j0 += 32) {
@@ -401,8 +405,7 @@ cudaError_t launch_dw(const Params& p, const DecodeLaunch& dl, const CUtensorMap
   auto kern = k2_decode<D, NCW>;
   cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(kern), dl.smem);
   if (e != cudaSuccess) return e;
-  kern<<<dl.grid, (NCW + kNP) * 32, dl.smem, stream>>>(tmK, tmV, p, dl.stages);
-  return cudaGetLastError();
+  return launch_pdl(kern, dim3(dl.grid), dim3((NCW + kNP) * 32), dl.smem, stream, tmK, tmV, p, dl.stages);
 }
 
 template <int D>

@@ -32,6 +32,7 @@ __global__ void __launch_bounds__(64 * kMaxGroups) k3_reduce(Params p) {
   __shared__ float s_max[kMaxGroups][8];
   __shared__ float4 s_num[kMaxGroups][8][8];
   __shared__ float s_den[kMaxGroups][8];
+  pdl_wait();  // the decode kernel's partials are complete and visible
   const int ny = p.Hkv * p.HG, nz = D / 32;
   const int n_items = p.B * ny * nz;
   for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
@@ -109,12 +110,10 @@ __global__ void __launch_bounds__(64 * kMaxGroups) k3_reduce(Params p) {
 template <typename T, int G>
 cudaError_t launch_reduce_g(const Params& p, int grid, cudaStream_t stream) {
   if (p.D == 64)
-    k3_reduce<T, 64, G><<<grid, 64 * G, 0, stream>>>(p);
-  else if (p.D == 128)
-    k3_reduce<T, 128, G><<<grid, 64 * G, 0, stream>>>(p);
-  else
-    return cudaErrorInvalidValue;
-  return cudaGetLastError();
+    return launch_pdl(k3_reduce<T, 64, G>, dim3(grid), dim3(64 * G), 0, stream, p);
+  if (p.D == 128)
+    return launch_pdl(k3_reduce<T, 128, G>, dim3(grid), dim3(64 * G), 0, stream, p);
+  return cudaErrorInvalidValue;
 }
 
 // Up to 4 segment groups (256 threads) when sequences may have many segments: long contexts

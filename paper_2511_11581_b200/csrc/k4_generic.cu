@@ -37,6 +37,7 @@ __global__ void __launch_bounds__(kWarps * 32) k4_generic(Params p) {
   const T* __restrict__ V = static_cast<const T*>(p.v);
   T* __restrict__ O = static_cast<T*>(p.out);
 
+  pdl_wait();  // K5's metadata is complete and visible
   const int total_qb = p.hdr[kHdrTotalQBlocks];
   const int n_pre = total_qb * p.Hkv;
   // decode segments (split-KV) when the decode kernel K2 cannot take them: one item
@@ -207,8 +208,7 @@ cudaError_t launch_t(const Params& p, int grid, cudaStream_t stream) {
   auto kern = k4_generic<T, D, RPW>;
   cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
   if (e != cudaSuccess) return e;
-  kern<<<grid, kWarps * 32, smem, stream>>>(p);
-  return cudaGetLastError();
+  return launch_pdl(kern, dim3(grid), dim3(kWarps * 32), smem, stream, p);
 }
 
 template <typename T, int D>

@@ -75,6 +75,7 @@ __device__ int2 block_exclusive_scan2(int2 v, int2* s_warp, int2* total) {
 // One CTA of min(1024, roundup(B, 32)) threads; sequence b is handled by thread b % blockDim
 // (one pass over the batch when B <= blockDim: per-sequence values stay in registers).
 __global__ void __launch_bounds__(kMaxThreads) k5_metadata(Params p) {
+  pdl_trigger();  // the next kernel may be scheduled now; it waits for this grid (pdl_wait)
   __shared__ unsigned long long s_red[32];
   __shared__ int2 s_scan[32];
   const int B = p.B;

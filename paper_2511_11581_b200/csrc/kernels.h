@@ -3,6 +3,9 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+#include <utility>
+
 #include "params.h"
 
 namespace pattn {
@@ -10,6 +13,29 @@ namespace pattn {
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device, size) instead of
 // on every launch (pattn_api.cu).
 cudaError_t ensure_dynamic_smem(const void* func, size_t bytes);
+
+// Launch with programmatic stream serialization (PDL) unless PATTN_NO_PDL is set: the kernel
+// may be scheduled while its stream predecessor finishes; it calls pdl_wait() before reading
+// the predecessor's results.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                       Args&&... args) {
+  static const bool off = [] {
+    const char* v = getenv("PATTN_NO_PDL");
+    return v && *v && *v != '0';
+  }();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = off ? 0 : 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 // K5: batch metadata + decode segment plan (one CTA).
 cudaError_t launch_metadata(const Params& p, cudaStream_t stream);
