@@ -138,7 +138,7 @@ def kernel_work(w):
     """Algorithmic work per step: causally visible (row,key) pairs
     only; KV bytes read once per (sequence, KV head)."""
     a = w.algorithmic()
-    D, Hq, esz = w.head_dim, w.num_q_heads, 2 if w.dtype == "bf16" else 4
+    D, Hq, esz = w.head_dim, w.num_q_heads, 4 if w.dtype == "f32" else 2
     n_dec = sum(1 for _, q in w.seqs if q == 1)
     n_pre_tok = sum(q for _, q in w.seqs if q > 1)
     return dict(
@@ -691,7 +691,7 @@ def main():
         "higher_is_better": True,
         "scaling": "weak" if args.shard == "none" else "strong",
         "vs_baseline": None,
-        "dtype": "bf16" if w.dtype == "bf16" else "f32",
+        "dtype": w.dtype,
         "data": "synthetic",
         "config": {
             "workload": args.workload,

@@ -74,7 +74,8 @@ typedef enum pattn_status {
 
 typedef enum pattn_dtype {
   PATTN_DTYPE_F32 = 0,  /* q, caches and out are fp32; exact-ish SIMT path (tol 1e-5) */
-  PATTN_DTYPE_BF16 = 1  /* q, caches and out are bf16; fp32 accumulation (tol 1e-2 abs + 1e-2 rel) */
+  PATTN_DTYPE_BF16 = 1, /* q, caches and out are bf16; fp32 accumulation (tol 1e-2 abs + 1e-2 rel) */
+  PATTN_DTYPE_F16 = 2   /* q, caches and out are fp16; the bf16 paths with fp16 storage (same tolerance) */
 } pattn_dtype_t;
 
 /*

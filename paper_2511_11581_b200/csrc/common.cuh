@@ -7,6 +7,7 @@
 
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <cstdio>
@@ -39,6 +40,23 @@ template <>
 PATTN_DEVICE float from_f32<float>(float x) { return x; }
 template <>
 PATTN_DEVICE __nv_bfloat16 from_f32<__nv_bfloat16>(float x) { return __float2bfloat16_rn(x); }
+// fp16 (PATTN_DTYPE_F16): same paths as bf16 with fp16 storage
+PATTN_DEVICE uint32_t pack_f16(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;\n" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+template <>
+PATTN_DEVICE float to_f32<__half>(__half x) { return __half2float(x); }
+template <>
+PATTN_DEVICE __half from_f32<__half>(float x) { return __float2half_rn(x); }
+// two fp32 -> one packed 16-bit pair (low half = lo), round to nearest even
+template <typename T>
+PATTN_DEVICE uint32_t pack2(float lo, float hi);
+template <>
+PATTN_DEVICE uint32_t pack2<__nv_bfloat16>(float lo, float hi) { return pack_bf16(lo, hi); }
+template <>
+PATTN_DEVICE uint32_t pack2<__half>(float lo, float hi) { return pack_f16(lo, hi); }
 
 PATTN_DEVICE float fast_exp2(float x) {
   float y;
@@ -279,6 +297,15 @@ PATTN_DEVICE uint32_t movmatrix_trans(uint32_t x) {
   asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;\n" : "=r"(y) : "r"(x));
   return y;
 }
+// D(16x8 f32) += A(16x16 f16, row) * B(16x8 f16, col)
+PATTN_DEVICE void mma_f16_16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+      "{%0, %1, %2, %3};\n"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
 // D(16x8 f32) += A(16x16 bf16, row) * B(16x8 bf16, col)
 PATTN_DEVICE void mma_bf16_16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
                                  uint32_t b1) {
@@ -366,16 +393,40 @@ PATTN_DEVICE uint64_t smem_desc_sw128(uint32_t start, uint32_t lbo, uint32_t sbo
   d |= (uint64_t)2u << 61;  // SWIZZLE_128B
   return d;
 }
-// Instruction descriptor, kind::f16: bf16 x bf16 -> f32, M x N, A/B major (0 = K-major, 1 = MN-major).
-__host__ __device__ constexpr uint32_t idesc_bf16_f32(int M, int N, int a_mn_major, int b_mn_major) {
+// Instruction descriptor, kind::f16: {bf16 | f16} x {bf16 | f16} -> f32, M x N, A/B major
+// (0 = K-major, 1 = MN-major); ab_fmt 1 = bf16, 0 = f16.
+__host__ __device__ constexpr uint32_t idesc_f16kind_f32(int M, int N, int a_mn_major, int b_mn_major,
+                                                         uint32_t ab_fmt) {
   return (1u << 4)                          // D format f32
-         | (1u << 7)                        // A bf16
-         | (1u << 10)                       // B bf16
+         | (ab_fmt << 7)                    // A format
+         | (ab_fmt << 10)                   // B format
          | ((uint32_t)a_mn_major << 15)     // A major
          | ((uint32_t)b_mn_major << 16)     // B major
          | ((uint32_t)(N >> 3) << 17)       // N / 8
          | ((uint32_t)(M >> 4) << 24);      // M / 16
 }
+
+
+// 16-bit element traits of the tensor-core paths (K1, K2): storage type, UMMA format code,
+// the packed conversion of P / outputs, and the mma.sync variant.
+struct EltBf16 {
+  using T = __nv_bfloat16;
+  static constexpr uint32_t kUmmaFmt = 1;
+  static PATTN_DEVICE uint32_t pack(float lo, float hi) { return pack_bf16(lo, hi); }
+  static PATTN_DEVICE void mma(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                               uint32_t b1) {
+    mma_bf16_16816(d, a0, a1, a2, a3, b0, b1);
+  }
+};
+struct EltF16 {
+  using T = __half;
+  static constexpr uint32_t kUmmaFmt = 0;
+  static PATTN_DEVICE uint32_t pack(float lo, float hi) { return pack_f16(lo, hi); }
+  static PATTN_DEVICE void mma(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                               uint32_t b1) {
+    mma_f16_16816(d, a0, a1, a2, a3, b0, b1);
+  }
+};
 
 }  // namespace pattn
 

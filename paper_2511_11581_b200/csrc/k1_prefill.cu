@@ -221,7 +221,7 @@ PATTN_DEVICE Item next_item(Bars& bar, const ItemSlot* ring, uint32_t n, int lan
   return x;
 }
 
-template <int D>
+template <int D, typename E>
 __global__ void __launch_bounds__(kThreads, 1)
     k1_prefill(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmO,
                const __grid_constant__ KvHeadMaps maps, Params p) {
@@ -358,8 +358,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kRegWG3) : "memory");  // warpgroup 3
     const int h_lo = warp == 15 ? 1 : 0;
     const int h_hi = h_lo + 1;
-    constexpr uint32_t idS = idesc_bf16_f32(kHalfM, kN, 0, 0);   // Q (K-major) x K (K-major)
-    constexpr uint32_t idPV = idesc_bf16_f32(kHalfM, D, 0, 1);  // P (TMEM, K-major) x V (MN-major)
+    constexpr uint32_t idS = idesc_f16kind_f32(kHalfM, kN, 0, 0, E::kUmmaFmt);   // Q (K-major) x K (K-major)
+    constexpr uint32_t idPV = idesc_f16kind_f32(kHalfM, D, 0, 1, E::kUmmaFmt);  // P (TMEM, K-major) x V (MN-major)
     // smem descriptors: start-address field = addr >> 4, so desc(base + off) = desc(base) + (off >> 4)
     const uint64_t dQ = smem_desc_sw128(sbase + kOffQ, 16, 1024);
     const uint64_t dK = smem_desc_sw128(sbase + kOffK, 16, kGroup);     // 8-key groups kGroup apart
@@ -508,7 +508,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t tc = 0, vc = 0;  // tiles seen by this warpgroup (== PV count of this half)
     uint32_t sc0 = 0u, sc1 = 0u;  // completed phases observed per S buffer (scalars: a runtime-indexed
                                   // array would live in local memory inside the tile loop)
-    __nv_bfloat16* O = static_cast<__nv_bfloat16*>(p.out);
+    using OutT = typename E::T;
+    OutT* O = static_cast<OutT*>(p.out);
     const float cs = p.scale_log2;
     const float ca = fmaxf(fabsf(cs), 1e-30f);  // scale 0: -inf * 0 would be NaN; 1e-30 * s ~ 0
     uint32_t ic = 0;
@@ -576,7 +577,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint64_t xx = ffma2(f32x2(s[c], s[c + 1]), ca2, nb2);
           const float e0 = fast_exp2(f32x2_lo(xx)), e1 = fast_exp2(f32x2_hi(xx));
           rs2[(c >> 1) & 3] = fadd2(rs2[(c >> 1) & 3], f32x2(e0, e1));
-          pk[c >> 1] = pack_bf16(e0, e1);
+          pk[c >> 1] = E::pack(e0, e1);
         }
         const uint64_t r01 = fadd2(rs2[0], rs2[1]), r23 = fadd2(rs2[2], rs2[3]), rr = fadd2(r01, r23);
         const float rs = f32x2_lo(rr) + f32x2_hi(rr);
@@ -665,13 +666,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int c0 = pass * 64 + c * 8;
             uint4 v;
             uint64_t a = fmul2((uint64_t)o[c0 + 0] | ((uint64_t)o[c0 + 1] << 32), inv2);
-            v.x = pack_bf16(f32x2_lo(a), f32x2_hi(a));
+            v.x = E::pack(f32x2_lo(a), f32x2_hi(a));
             a = fmul2((uint64_t)o[c0 + 2] | ((uint64_t)o[c0 + 3] << 32), inv2);
-            v.y = pack_bf16(f32x2_lo(a), f32x2_hi(a));
+            v.y = E::pack(f32x2_lo(a), f32x2_hi(a));
             a = fmul2((uint64_t)o[c0 + 4] | ((uint64_t)o[c0 + 5] << 32), inv2);
-            v.z = pack_bf16(f32x2_lo(a), f32x2_hi(a));
+            v.z = E::pack(f32x2_lo(a), f32x2_hi(a));
             a = fmul2((uint64_t)o[c0 + 6] | ((uint64_t)o[c0 + 7] << 32), inv2);
-            v.w = pack_bf16(f32x2_lo(a), f32x2_hi(a));
+            v.w = E::pack(f32x2_lo(a), f32x2_hi(a));
             *reinterpret_cast<uint4*>(stg + row_off + ((c ^ (r & 7)) << 4)) = v;
           }
           fence_proxy_async_smem();
@@ -682,19 +683,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       } else if (row_valid) {
-        __nv_bfloat16* orow = O + (int64_t)(x.q0 + x.tok0 + tk) * p.o_st_tok +
+        OutT* orow = O + (int64_t)(x.q0 + x.tok0 + tk) * p.o_st_tok +
                               (int64_t)(x.kvh * G + (r % G)) * p.o_st_head;
 #pragma unroll
         for (int c = 0; c < D; c += 8) {
           uint4 v;
           uint64_t a = fmul2((uint64_t)o[c + 0] | ((uint64_t)o[c + 1] << 32), inv2);
-          v.x = pack_bf16(f32x2_lo(a), f32x2_hi(a));
+          v.x = E::pack(f32x2_lo(a), f32x2_hi(a));
           a = fmul2((uint64_t)o[c + 2] | ((uint64_t)o[c + 3] << 32), inv2);
-          v.y = pack_bf16(f32x2_lo(a), f32x2_hi(a));
+          v.y = E::pack(f32x2_lo(a), f32x2_hi(a));
           a = fmul2((uint64_t)o[c + 4] | ((uint64_t)o[c + 5] << 32), inv2);
-          v.z = pack_bf16(f32x2_lo(a), f32x2_hi(a));
+          v.z = E::pack(f32x2_lo(a), f32x2_hi(a));
           a = fmul2((uint64_t)o[c + 6] | ((uint64_t)o[c + 7] << 32), inv2);
-          v.w = pack_bf16(f32x2_lo(a), f32x2_hi(a));
+          v.w = E::pack(f32x2_lo(a), f32x2_hi(a));
           *reinterpret_cast<uint4*>(orow + c) = v;
         }
       }
@@ -731,7 +732,8 @@ PrefillLaunch plan_prefill(const Params& p, int num_sms) {
 
 cudaError_t launch_prefill(const Params& p, const PrefillLaunch& pl, const CUtensorMap& tmQ, const CUtensorMap& tmO,
                            const KvHeadMaps& kv, cudaStream_t stream) {
-  auto kern = p.D == 64 ? k1_prefill<64> : k1_prefill<128>;
+  auto kern = p.dtype == 2 ? (p.D == 64 ? k1_prefill<64, EltF16> : k1_prefill<128, EltF16>)
+                           : (p.D == 64 ? k1_prefill<64, EltBf16> : k1_prefill<128, EltBf16>);
   cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(kern), pl.smem);
   if (e != cudaSuccess) return e;
   return launch_pdl(kern, dim3(pl.grid), dim3(kThreads), pl.smem, stream, tmQ, tmO, kv, p);

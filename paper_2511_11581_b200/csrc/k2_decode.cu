@@ -90,7 +90,7 @@ __device__ __forceinline__ Item decode_item(const Params& p, int it) {
   return x;
 }
 
-template <int D, int NCW>
+template <int D, int NCW, typename E>
 __global__ void __launch_bounds__((NCW + kNP) * 32, 1)
     k2_decode(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, Params p,
               int nst) {
@@ -213,8 +213,9 @@ __global__ void __launch_bounds__((NCW + kNP) * 32, 1)
   const int r = lane >> 2, c = lane & 3;       // mma fragment coordinates
   const int mat = lane >> 3, mrow = lane & 7;  // ldmatrix source coordinates
   float* scr = scratch + cw * kScr;
-  __nv_bfloat16* O = static_cast<__nv_bfloat16*>(p.out);
-  const __nv_bfloat16* Q = static_cast<const __nv_bfloat16*>(p.q);
+  using ET = typename E::T;
+  ET* O = static_cast<ET*>(p.out);
+  const ET* Q = static_cast<const ET*>(p.q);
   const uint32_t ring_u32 = smem_u32(ring);
   uint32_t g = 0;
 
@@ -234,7 +235,7 @@ __global__ void __launch_bounds__((NCW + kNP) * 32, 1)
     // Q^T as the B operand of S^T = K . Q^T: b0 = Q[head r][16kc + 2c .. +1], b1 = +8
     uint32_t bq[S::kKC][2];
     {
-      const __nv_bfloat16* qrow = Q + (int64_t)x.tok * p.q_st_tok + (int64_t)(head0 + r) * p.q_st_head;
+      const ET* qrow = Q + (int64_t)x.tok * p.q_st_tok + (int64_t)(head0 + r) * p.q_st_head;
 #pragma unroll
       for (int kc = 0; kc < S::kKC; ++kc) {
         bq[kc][0] = r < g_eff ? __ldg(reinterpret_cast<const uint32_t*>(qrow + kc * 16 + 2 * c)) : 0u;
@@ -269,7 +270,7 @@ __global__ void __launch_bounds__((NCW + kNP) * 32, 1)
         const uint32_t addr = kq + (dd >> 6) * S::kHalfBytes + key * 128 + ((((dd & 63) >> 3) ^ (key & 7)) << 4);
         uint32_t a0, a1, a2, a3;
         ldmatrix_x4(addr, a0, a1, a2, a3);
-        mma_bf16_16816(sc, a0, a1, a2, a3, bq[kc][0], bq[kc][1]);
+        E::mma(sc, a0, a1, a2, a3, bq[kc][0], bq[kc][1]);
       }
     };
     for (int j = cw; j < nsb; j += NCW) {
@@ -320,8 +321,8 @@ __global__ void __launch_bounds__((NCW + kNP) * 32, 1)
         acc[t][3] *= al1;
       }
       // P^T as the B operand of O^T = V^T . P^T (transpose the 8x8 halves in registers)
-      const uint32_t pb0 = movmatrix_trans(pack_bf16(p0, p1));
-      const uint32_t pb1 = movmatrix_trans(pack_bf16(p2, p3));
+      const uint32_t pb0 = movmatrix_trans(E::pack(p0, p1));
+      const uint32_t pb1 = movmatrix_trans(E::pack(p2, p3));
 #pragma unroll
       for (int t = 0; t < S::kKC; ++t) {
         const int key = (mat >> 1) * 8 + mrow;
@@ -329,7 +330,7 @@ __global__ void __launch_bounds__((NCW + kNP) * 32, 1)
         const uint32_t addr = vst + (dd >> 6) * S::kHalfBytes + key * 128 + ((((dd & 63) >> 3) ^ (key & 7)) << 4);
         uint32_t a0, a1, a2, a3;
         ldmatrix_x4_trans(addr, a0, a1, a2, a3);
-        mma_bf16_16816(acc[t], a0, a1, a2, a3, pb0, pb1);
+        E::mma(acc[t], a0, a1, a2, a3, pb0, pb1);
       }
       __syncwarp();
       if (valid < kSub) fence_proxy_async_smem();  // generic zero-writes before the next TMA fill
@@ -381,7 +382,7 @@ __global__ void __launch_bounds__((NCW + kNP) * 32, 1)
         den = fmaf(wt, scratch[w * kScr + 8 + h], den);
       }
       if (x.nseg == 1) {
-        O[(int64_t)x.tok * p.o_st_tok + (int64_t)(head0 + h) * p.o_st_head + d] = __float2bfloat16_rn(num / den);
+        O[(int64_t)x.tok * p.o_st_tok + (int64_t)(head0 + h) * p.o_st_head + d] = from_f32<ET>(num / den);
       } else {
         const int64_t row = (int64_t)x.c * p.Hq + head0 + h;
         p.part_acc[row * D + d] = num;
@@ -399,10 +400,10 @@ __global__ void __launch_bounds__((NCW + kNP) * 32, 1)
 
 int env_or(const char* name, int dflt);
 
-template <int D, int NCW>
+template <int D, int NCW, typename E>
 cudaError_t launch_dw(const Params& p, const DecodeLaunch& dl, const CUtensorMap& tmK, const CUtensorMap& tmV,
                       cudaStream_t stream) {
-  auto kern = k2_decode<D, NCW>;
+  auto kern = k2_decode<D, NCW, E>;
   cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(kern), dl.smem);
   if (e != cudaSuccess) return e;
   return launch_pdl(kern, dim3(dl.grid), dim3((NCW + kNP) * 32), dl.smem, stream, tmK, tmV, p, dl.stages);
@@ -411,8 +412,12 @@ cudaError_t launch_dw(const Params& p, const DecodeLaunch& dl, const CUtensorMap
 template <int D>
 cudaError_t launch_d(const Params& p, const DecodeLaunch& dl, const CUtensorMap& tmK, const CUtensorMap& tmV,
                      cudaStream_t stream) {
-  if (dl.consumer_warps == 8) return launch_dw<D, 8>(p, dl, tmK, tmV, stream);
-  return launch_dw<D, 4>(p, dl, tmK, tmV, stream);
+  if (p.dtype == 2) {
+    if (dl.consumer_warps == 8) return launch_dw<D, 8, EltF16>(p, dl, tmK, tmV, stream);
+    return launch_dw<D, 4, EltF16>(p, dl, tmK, tmV, stream);
+  }
+  if (dl.consumer_warps == 8) return launch_dw<D, 8, EltBf16>(p, dl, tmK, tmV, stream);
+  return launch_dw<D, 4, EltBf16>(p, dl, tmK, tmV, stream);
 }
 
 int env_or(const char* name, int dflt) {

@@ -94,8 +94,8 @@ __global__ void __launch_bounds__(64 * kMaxGroups) k3_reduce(Params p) {
       T* O = static_cast<T*>(p.out) + (int64_t)tok * p.o_st_tok + (int64_t)(head0 + h) * p.o_st_head + d4g * 4;
       if constexpr (sizeof(T) == 2) {
         uint2 packed;
-        packed.x = pack_bf16(t.x * inv, t.y * inv);
-        packed.y = pack_bf16(t.z * inv, t.w * inv);
+        packed.x = pack2<T>(t.x * inv, t.y * inv);
+        packed.y = pack2<T>(t.z * inv, t.w * inv);
         *reinterpret_cast<uint2*>(O) = packed;
       } else {
         *reinterpret_cast<float4*>(O) = make_float4(t.x * inv, t.y * inv, t.z * inv, t.w * inv);
@@ -128,7 +128,8 @@ cudaError_t launch_reduce_t(const Params& p, cudaStream_t stream) {
 }
 
 cudaError_t launch_reduce(const Params& p, cudaStream_t stream) {
-  return p.dtype == 0 ? launch_reduce_t<float>(p, stream) : launch_reduce_t<__nv_bfloat16>(p, stream);
+  if (p.dtype == 0) return launch_reduce_t<float>(p, stream);
+  return p.dtype == 2 ? launch_reduce_t<__half>(p, stream) : launch_reduce_t<__nv_bfloat16>(p, stream);
 }
 
 }  // namespace pattn

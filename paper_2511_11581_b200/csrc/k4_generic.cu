@@ -228,6 +228,10 @@ cudaError_t launch_generic(const Params& p, int grid, int rows_per_warp, cudaStr
     if (p.D == 64) return launch_d<float, 64>(p, grid, rows_per_warp, stream);
     if (p.D == 128) return launch_d<float, 128>(p, grid, rows_per_warp, stream);
   } else {
+    if (p.dtype == 2) {
+      if (p.D == 64) return launch_d<__half, 64>(p, grid, rows_per_warp, stream);
+      if (p.D == 128) return launch_d<__half, 128>(p, grid, rows_per_warp, stream);
+    }
     if (p.D == 64) return launch_d<__nv_bfloat16, 64>(p, grid, rows_per_warp, stream);
     if (p.D == 128) return launch_d<__nv_bfloat16, 128>(p, grid, rows_per_warp, stream);
   }

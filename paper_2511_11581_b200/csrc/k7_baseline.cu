@@ -38,6 +38,14 @@ template <>
 __device__ __forceinline__ void st_from_f32<__nv_bfloat16>(__nv_bfloat16* p, float x) {
   *p = __float2bfloat16_rn(x);
 }
+template <>
+__device__ __forceinline__ float ld_f32<__half>(const __half* p) {
+  return __half2float(__ldg(p));
+}
+template <>
+__device__ __forceinline__ void st_from_f32<__half>(__half* p, float x) {
+  *p = __float2half_rn(x);
+}
 
 template <typename T, int D>
 __global__ void __launch_bounds__(128) k7_baseline(Params p) {
@@ -119,6 +127,7 @@ cudaError_t launch_t(const Params& p, cudaStream_t stream) {
 
 cudaError_t launch_baseline(const Params& p, cudaStream_t stream) {
   if (p.T == 0) return cudaSuccess;
+  if (p.dtype == 2) return launch_t<__half>(p, stream);
   return p.dtype == 1 ? launch_t<__nv_bfloat16>(p, stream) : launch_t<float>(p, stream);
 }
 

@@ -191,7 +191,8 @@ pattn_status_t check_problem(const pattn_problem_t* p) {
     return PATTN_ERR_INVALID_ARG;
   if (p->num_q_heads % p->num_kv_heads != 0) return PATTN_ERR_INVALID_ARG;
   if (p->head_dim != 64 && p->head_dim != 128) return PATTN_ERR_UNSUPPORTED;
-  if (p->dtype != PATTN_DTYPE_F32 && p->dtype != PATTN_DTYPE_BF16) return PATTN_ERR_UNSUPPORTED;
+  if (p->dtype != PATTN_DTYPE_F32 && p->dtype != PATTN_DTYPE_BF16 && p->dtype != PATTN_DTYPE_F16)
+    return PATTN_ERR_UNSUPPORTED;
   if (p->num_q_heads / p->num_kv_heads > 64) return PATTN_ERR_UNSUPPORTED;
   if (p->q_stride_tok <= 0 || p->q_stride_head <= 0 || p->kv_stride_blk <= 0 || p->kv_stride_tok <= 0 ||
       p->kv_stride_head <= 0 || p->bt_stride < p->max_blocks_per_seq || p->o_stride_tok <= 0 ||
@@ -245,7 +246,7 @@ pattn_status_t make_plan(const pattn_problem_t* p, const void* q, const void* kc
   pl->max_smem = di.ok ? di.max_smem : 227 * 1024;
   const int G = p->num_q_heads / p->num_kv_heads;
   const int D = p->head_dim;
-  const bool bf16 = p->dtype == PATTN_DTYPE_BF16;
+  const bool bf16 = p->dtype == PATTN_DTYPE_BF16 || p->dtype == PATTN_DTYPE_F16;  // 16-bit: tensor-core paths
   const bool generic = (p->flags & PATTN_FLAG_FORCE_GENERIC) != 0;
   pl->HG = (G + 7) / 8;
   pl->kv_tok_inner = p->kv_stride_tok < p->kv_stride_head;
@@ -340,6 +341,10 @@ pattn_status_t make_plan(const pattn_problem_t* p, const void* q, const void* kc
   return PATTN_OK;
 }
 
+CUtensorMapDataType tma_dtype(const pattn_problem_t* p) {
+  return p->dtype == PATTN_DTYPE_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+}
+
 // H2: per-KV-head 5-D views for K1 {64 d, 8 slots, 2 d-halves, bs/8 slot groups, block}
 // (the head is folded into the base address; strides deliberately not nested) so that one
 // box {64, 8, 2, 2, 1} brings a 16-key sub-block in the [group][half][8][64] order UMMA
@@ -354,7 +359,7 @@ bool encode_head_map(CUtensorMap* tm, const pattn_problem_t* p, const void* head
                            (cuuint64_t)p->kv_stride_blk * 2};
   cuuint32_t box[5] = {64, 8, (cuuint32_t)(p->head_dim / 64), 2, 1};
   cuuint32_t estr[5] = {1, 1, 1, 1, 1};
-  CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(head_base), dims, strides, box, estr,
+  CUresult r = fn(tm, tma_dtype(p), 5, const_cast<void*>(head_base), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
@@ -372,7 +377,8 @@ struct HeadMapCache {
 bool encode_head_maps(KvHeadMaps* out, const pattn_problem_t* p, const void* kc, const void* vc) {
   static HeadMapCache cache;
   std::lock_guard<std::mutex> lock(cache.mu);
-  const bool hit = cache.valid && cache.k == kc && cache.v == vc && cache.prob.num_kv_heads == p->num_kv_heads &&
+  const bool hit = cache.valid && cache.k == kc && cache.v == vc && cache.prob.dtype == p->dtype &&
+                   cache.prob.num_kv_heads == p->num_kv_heads &&
                    cache.prob.head_dim == p->head_dim && cache.prob.block_size == p->block_size &&
                    cache.prob.num_blocks == p->num_blocks && cache.prob.kv_stride_blk == p->kv_stride_blk &&
                    cache.prob.kv_stride_tok == p->kv_stride_tok && cache.prob.kv_stride_head == p->kv_stride_head;
@@ -408,7 +414,7 @@ bool encode_kv_map5(CUtensorMap* tm, const pattn_problem_t* p, const void* base)
                            (cuuint64_t)p->kv_stride_blk * 2};
   cuuint32_t box[5] = {64, 16, (cuuint32_t)halves, 1, 1};
   cuuint32_t estr[5] = {1, 1, 1, 1, 1};
-  CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base), dims, strides, box, estr,
+  CUresult r = fn(tm, tma_dtype(p), 5, const_cast<void*>(base), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
@@ -426,7 +432,7 @@ bool encode_q_map(CUtensorMap* tm, const pattn_problem_t* p, const void* q, int 
                            (cuuint64_t)p->q_stride_tok * 2};
   cuuint32_t box[4] = {64, (cuuint32_t)G, 1, (cuuint32_t)(block_q / 2)};  // one 128-row half
   cuuint32_t estr[4] = {1, 1, 1, 1};
-  CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(q), dims, strides, box, estr,
+  CUresult r = fn(tm, tma_dtype(p), 4, const_cast<void*>(q), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
@@ -445,7 +451,7 @@ bool encode_o_map(CUtensorMap* tm, const pattn_problem_t* p, void* out) {
                            (cuuint64_t)p->o_stride_tok * 2};
   cuuint32_t box[4] = {64, (cuuint32_t)G, 1, (cuuint32_t)(32 / G)};
   cuuint32_t estr[4] = {1, 1, 1, 1};
-  CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, out, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+  CUresult r = fn(tm, tma_dtype(p), 4, out, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -794,11 +800,12 @@ pattn_status_t pattn_write_kv(const pattn_problem_t* p, const void* k_new, const
       p->max_blocks_per_seq <= 0 || p->bt_stride < p->max_blocks_per_seq || new_stride_tok <= 0 ||
       new_stride_head <= 0 || p->kv_stride_blk <= 0 || p->kv_stride_tok <= 0 || p->kv_stride_head <= 0)
     return PATTN_ERR_INVALID_ARG;
-  if (p->dtype != PATTN_DTYPE_F32 && p->dtype != PATTN_DTYPE_BF16) return PATTN_ERR_UNSUPPORTED;
+  if (p->dtype != PATTN_DTYPE_F32 && p->dtype != PATTN_DTYPE_BF16 && p->dtype != PATTN_DTYPE_F16)
+    return PATTN_ERR_UNSUPPORTED;
   if (p->num_tokens == 0) return PATTN_OK;
   if (!k_new || !v_new || !k_cache || !v_cache || !block_table || !cu_seqlens_q || !seq_lens)
     return PATTN_ERR_INVALID_ARG;
-  const int64_t esz = p->dtype == PATTN_DTYPE_BF16 ? 2 : 4;
+  const int64_t esz = p->dtype == PATTN_DTYPE_F32 ? 4 : 2;
   WriteKvParams w{};
   w.k_new = k_new;
   w.v_new = v_new;

@@ -31,7 +31,7 @@ STATUS = {
     6: "PATTN_ERR_WORKSPACE_TOO_SMALL",
     7: "PATTN_ERR_CUDA",
 }
-DTYPE_F32, DTYPE_BF16 = 0, 1
+DTYPE_F32, DTYPE_BF16, DTYPE_F16 = 0, 1, 2
 FLAG_FORCE_GENERIC, FLAG_NO_SPLIT, FLAG_FORCE_SPLIT, FLAG_SERIAL, FLAG_BASELINE = 0x1, 0x2, 0x4, 0x8, 0x10
 KERNEL_METADATA, KERNEL_PREFILL, KERNEL_DECODE, KERNEL_REDUCE, KERNEL_GENERIC, KERNEL_BASELINE, KERNEL_COUNT = range(7)
 KERNEL_NAMES = ["metadata", "prefill", "decode", "reduce", "generic", "baseline"]
@@ -173,6 +173,8 @@ def _dtype_code(t: torch.Tensor) -> int:
         return DTYPE_F32
     if t.dtype == torch.bfloat16:
         return DTYPE_BF16
+    if t.dtype == torch.float16:
+        return DTYPE_F16
     raise PattnError(5, f"dtype {t.dtype}")
 
 

@@ -68,6 +68,9 @@ CASES = [
     ((32, 8), 128, 80, "bf16", "NHD", "peaked"),   # bs 80 on the tcgen05 prefill path (G = 4)
     ((64, 8), 128, 48, "bf16", "HND", "peaked"),   # bs 48: 3 sub-blocks per paged block, G = 8
     ((8, 8), 128, 128, "bf16", "NHD", "peaked"),   # bs 128, G = 1 (BLOCK_Q = 256 tokens)
+    ((32, 8), 128, 16, "f16", "NHD", "peaked"),    # fp16 storage: K1 / K2 / K3 with f16 operands
+    ((64, 8), 128, 80, "f16", "HND", "uniform"),
+    ((8, 8), 64, 7, "f16", "NHD", "peaked"),       # fp16, bs 7: K4 with split decodes
 ]
 
 
@@ -404,6 +407,31 @@ def test_split_decode_on_generic_path(dt, bs, layout, flags):
     assert torch.equal(db.run(flags=flags), a)
 
 
+def test_fp16_tensor_core_paths_and_needle():
+    """fp16 storage (PATTN_DTYPE_F16) runs the same kernels as bf16 with f16 UMMA / mma.sync
+    operands: the tcgen05 prefill and the TMA decode are planned, the output matches the oracle,
+    and the needle case is bit-exact (P = 1 for the needle, exactly 0 elsewhere)."""
+    w = Workload("f16mix", ((0, 700), (5000, 1), (300, 90), (20000, 1), (9, 1)), 32, 8, 128, 16, "f16")
+    batch = generate(w, seed=51, dist="peaked", poison=True)
+    db = DeviceBatch(batch)
+    p = P.make_problem(db.q, db.k, 8, 16, db.bt, w.num_seqs, None, "NHD", 700, 20001)
+    assert P.planned_kernels(p) & (1 << P.KERNEL_PREFILL) and P.planned_kernels(p) & (1 << P.KERNEL_DECODE)
+    _check(batch, 0, "fp16 mixed")
+    _check(batch, P.FLAG_FORCE_SPLIT, "fp16 forced split")
+    wn = Workload("f16needle", ((700, 1), (0, 50), (1500, 1), (40, 20)), 32, 8, 128, 16, "f16")
+    nb = generate(wn, seed=7, dist="needle")
+    out = DeviceBatch(nb).run().cpu()
+    v = nb.v_cache
+    for b in range(wn.num_seqs):
+        s_, e_ = int(nb.cu_seqlens_q[b]), int(nb.cu_seqlens_q[b + 1])
+        for g in range(wn.num_kv_heads):
+            t = int(nb.needle_pos[b, g])
+            row = torch.from_numpy(np.ascontiguousarray(v[nb.block_table[b, t // 16], t % 16, g]))
+            for tok in range(s_, e_):
+                for h in range(g * 4, g * 4 + 4):
+                    assert torch.equal(out[tok, h], row), (b, g, tok, h)
+
+
 def test_hintless_call_matches_oracle():
     """No host hints (max_query_len / max_seq_len = 0): the planner uses its upper bounds."""
     w = Workload("nohint", ((0, 300), (2500, 1), (64, 40), (900, 1)), 32, 8, 128, 16, "bf16")
@@ -596,7 +624,8 @@ def test_shape_fuzz(i):
     heads = FUZZ_HEADS[int(rng.integers(len(FUZZ_HEADS)))]
     D = int(rng.choice([64, 128]))
     bs = int(rng.choice([16, 32, 48, 80, 128, 5, 7, 24]))
-    dt = "f32" if rng.random() < 0.2 else "bf16"
+    u = rng.random()
+    dt = "f32" if u < 0.2 else ("f16" if u < 0.4 else "bf16")
     layout = "HND" if rng.random() < 0.4 else "NHD"
     w = random_workload(rng, heads, D, bs, dt, max_seqs=7, max_len=int(rng.choice([300, 1200, 2500])),
                         decode_share=float(rng.uniform(0.2, 0.8)))

@@ -236,3 +236,11 @@ def test_widen_matches_torch_bf16_to_fp32():
     assert w[0] == 1.0 and w[1] == -2.0 and np.isinf(w[2]) and w[2] > 0 and w[3] == np.float32(2.0 ** -133)
     f = np.array([0.5, -3.25], np.float32)
     assert np.array_equal(widen(f), f)  # fp32 storage passes through unchanged
+    # fp16 storage (PATTN_DTYPE_F16): every pattern widened exactly, as torch converts it
+    h = bits.view(np.float16)
+    ours16 = widen(h)
+    ref16 = torch.from_numpy(h.copy()).float().numpy()
+    nan16 = np.isnan(ref16)
+    assert np.array_equal(np.isnan(ours16), nan16)
+    assert np.array_equal(ours16[~nan16].view(np.uint32), ref16[~nan16].view(np.uint32))
+    assert widen(np.array([1.0, 65504.0, 2.0 ** -24], np.float16)).tolist() == [1.0, 65504.0, 2.0 ** -24]

@@ -58,7 +58,7 @@ class Workload:
     num_kv_heads: int
     head_dim: int
     block_size: int
-    dtype: str  # "f32" | "bf16"
+    dtype: str  # "f32" | "bf16" | "f16"
 
     @property
     def scale(self) -> float:
@@ -143,7 +143,7 @@ ATTRIBUTION: Dict[str, Workload] = {
 class Batch:
     workload: Workload
     layout: str  # "NHD": [num_blocks, bs, Hkv, D]; "HND": [num_blocks, Hkv, bs, D]
-    q: np.ndarray  # [T, Hq, D]  float32 (f32) or uint16 bf16 bits (bf16)
+    q: np.ndarray  # [T, Hq, D]  float32 (f32), uint16 bf16 bits (bf16) or float16 (f16)
     k_cache: np.ndarray
     v_cache: np.ndarray
     block_table: np.ndarray  # int32 [B, max_blocks_per_seq], padded with -1
@@ -173,20 +173,23 @@ class Batch:
 def _uniform(rng: np.random.Generator, shape, dtype: str, mult: float = 1.0) -> np.ndarray:
     """U[-1,1]*mult drawn in fp32, rounded to the storage dtype (chunked to bound memory)."""
     n = int(np.prod(shape))
-    out = np.empty(n, dtype=np.uint16 if dtype == "bf16" else np.float32)
+    out = np.empty(n, dtype=np.uint16 if dtype == "bf16" else (np.float16 if dtype == "f16" else np.float32))
     chunk = 1 << 24
     for s in range(0, n, chunk):
         e = min(n, s + chunk)
         x = rng.random(e - s, dtype=np.float32)
         x *= np.float32(2.0 * mult)
         x -= np.float32(mult)
-        out[s:e] = f32_to_bf16_bits(x) if dtype == "bf16" else x
+        # fp16: numpy's float32 -> float16 cast rounds to nearest even
+        out[s:e] = f32_to_bf16_bits(x) if dtype == "bf16" else x.astype(out.dtype)
     return out.reshape(shape)
 
 
 def _const(shape, value: float, dtype: str) -> np.ndarray:
     if dtype == "bf16":
         return np.full(shape, f32_to_bf16_bits(np.array([value], np.float32))[0], dtype=np.uint16)
+    if dtype == "f16":
+        return np.full(shape, value, dtype=np.float16)
     return np.full(shape, value, dtype=np.float32)
 
 
@@ -253,7 +256,7 @@ def generate(
                 k[bt[b, t // bs], t % bs, g, :] = four
 
     if poison:
-        nan = BF16_NAN if dt == "bf16" else np.float32(np.nan)
+        nan = BF16_NAN if dt == "bf16" else (np.float16(np.nan) if dt == "f16" else np.float32(np.nan))
         used = np.zeros(num_blocks, dtype=bool)
         for b in range(B):
             used[bt[b, : nblk[b]]] = True
@@ -300,7 +303,7 @@ def generate_device(w: Workload, seed: int, device="cuda", layout: str = "NHD", 
     num_blocks = int(nblk.sum()) + spare_blocks
     max_blocks = max(1, int(nblk.max()))
     T = int(q_lens.sum())
-    tdt = torch.bfloat16 if w.dtype == "bf16" else torch.float32
+    tdt = {"bf16": torch.bfloat16, "f16": torch.float16}.get(w.dtype, torch.float32)
 
     def uni(shape):
         out = torch.empty(shape, dtype=tdt, device=device)
