@@ -466,26 +466,3 @@ PATTN_DEVICE uint64_t fmul2(uint64_t a, uint64_t b) {
   return d;
 }
 }  // namespace pattn
-
-namespace pattn {
-// 2^x for two fp32 lanes on the FMA / ALU pipes instead of the MUFU (XU) pipe: Cody-Waite split
-// x = j + f (j = floor(x) via a round-down add of 1.5 * 2^23, f in [0, 1)), 2^f by a degree-3
-// polynomial with p(0) = 1 (coefficients fitted for minimum relative error on [0, 1): max 8.6e-5,
-// below half a bf16 ulp), 2^j by adding j to the exponent field.  Inputs below -127 (including
-// -inf of masked scores) are clamped to -127, which returns exactly +0.
-PATTN_DEVICE uint64_t exp2_poly2(uint64_t x) {
-  const uint64_t xx = f32x2(fmaxf(f32x2_lo(x), -127.f), fmaxf(f32x2_hi(x), -127.f));
-  const uint64_t magic = f32x2(12582912.f, 12582912.f), nmagic = f32x2(-12582912.f, -12582912.f);
-  uint64_t t;
-  asm("add.rm.f32x2 %0, %1, %2;\n" : "=l"(t) : "l"(xx), "l"(magic));
-  const uint64_t j = fadd2(t, nmagic);                                   // floor(x), exact
-  const uint64_t f = ffma2(j, f32x2(-1.f, -1.f), xx);                    // x - floor(x)
-  uint64_t p = ffma2(f32x2(0.07705993f, 0.07705993f), f, f32x2(0.22765276f, 0.22765276f));
-  p = ffma2(p, f, f32x2(0.69511503f, 0.69511503f));
-  p = ffma2(p, f, f32x2(1.f, 1.f));
-  const uint32_t lo = ((uint32_t)t << 23) + (uint32_t)p;                  // low 9 bits of t = j (two's complement)
-  const uint32_t hi = ((uint32_t)(t >> 32) << 23) + (uint32_t)(p >> 32);
-  return (uint64_t)lo | ((uint64_t)hi << 32);
-}
-}  // namespace pattn
-

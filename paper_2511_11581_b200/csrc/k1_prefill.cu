@@ -78,10 +78,7 @@ namespace {
 
 constexpr int kHalfM = 128;    // rows per half (one UMMA M)
 constexpr int kM = 2 * kHalfM; // BLOCK_M
-// Keys per KV tile N (template parameter): 64 -> S double-buffered per half (4 x 64 TMEM columns),
-// 128 -> "ping-pong" schedule: one 128-column S buffer per half, S_h(j+1) issued right after
-// PV_h(j) (P aliased on S), so each half alternates softmax and tensor work and the two halves
-// interleave on the tensor pipe.
+constexpr int kN = 64;         // keys per KV tile
 constexpr int kThreads = 512;  // 16 warps
 // setmaxnreg budgets (16-warp layout): warpgroup 0 (producers, MMA a), warpgroups 1-2
 // (softmax), warpgroup 3 (V producer, scheduler, Q producer, MMA b); 128 (a + d) + 256 s = 65536
@@ -99,37 +96,33 @@ constexpr int kRegWG0 = PATTN_K1_REG_WG0, kRegSoftmax = PATTN_K1_REG_SOFTMAX, kR
 static_assert(128 * (kRegWG0 + kRegWG3) + 256 * kRegSoftmax <= 65536, "register budget");
 // K / V tile layout: sub-block i (16 keys) = [8-slot group g][d half h][8 slots][64 d], i.e.
 // 8-key group G = 2i+g at G*kGroup + h*1024 (SW128 atoms of 8 rows x 128 B); kGroup = 16*D B.
-constexpr int kMaxStages = 4;
-#ifndef PATTN_K1_POLY
-#define PATTN_K1_POLY 0
+#ifndef PATTN_K1_KST
+#define PATTN_K1_KST 3
 #endif
-constexpr int kPolyPairs = PATTN_K1_POLY;  // of every 8 exponential pairs, this many on the FMA pipe
+#ifndef PATTN_K1_VST
+#define PATTN_K1_VST 3
+#endif
+constexpr int kKStages = PATTN_K1_KST;
+constexpr int kVStages = PATTN_K1_VST;  // V waits on PV (later than S), so it gets the deeper ring
 constexpr float kRescaleThreshold = 8.0f;  // log2 domain: rescale O only if the max grows by > 2^8
 constexpr uint32_t kBarBlock = 512;        // barriers + the item ring
 
 // Head-dim dependent sizes and the shared-memory map (offsets from a 1024-aligned base).
-template <int D, int N>
+template <int D>
 struct K1Shape {
   static_assert(D == 64 || D == 128, "head_dim");
-  static_assert(N == 64 || N == 128, "KV tile");
-  static constexpr bool kPP = N == 128;                     // ping-pong schedule (single S buffer per half)
-  // ring depths in tiles: 64-key tiles 3 / 3; 128-key tiles at D = 128: 2 / 2 (32 KB stages)
-  static constexpr int kKStages = (kPP && D == 128) ? 2 : 3;
-  static constexpr int kVStages = kKStages;
   static constexpr int kHalves = D / 64;                   // 64-wide (128-byte) d halves
   static constexpr uint32_t kQTile = kHalfM * D * 2;       // one 128-row half of the Q block (32 / 16 KB)
   static constexpr uint32_t kHalf = kHalfM * 64 * 2;       // 16 KB: one 64-wide d half of a Q half
-  static constexpr uint32_t kTile = N * D * 2;             // one K or V tile (64 keys: 16 / 8 KB)
+  static constexpr uint32_t kTile = kN * D * 2;            // one K or V tile (64 keys: 16 / 8 KB)
   static constexpr uint32_t kSub16Bytes = 16 * D * 2;      // one 16-key sub-block (4 / 2 KB)
   static constexpr uint32_t kGroup = 8 * D * 2;            // one 8-key group (2 / 1 KB)
   static constexpr uint32_t kOffQ = 0;                     // half a, then half b
   static constexpr uint32_t kOffK = kOffQ + 2 * kQTile;
   static constexpr uint32_t kOffV = kOffK + kKStages * kTile;
   // epilogue staging, 128B-swizzled as the out TMA map expects: per warp 32 rows x 128 B per
-  // 64-wide d half, all halves staged at once (no read wait in between) -- except for 128-key
-  // tiles at D = 128 (two 32 KB K / V stages each), which stage one d half at a time
-  static constexpr int kStagePasses = (kPP && D == 128) ? 1 : kHalves;  // d halves staged at once
-  static constexpr uint32_t kStageWarp = 4096 * kStagePasses;
+  // 64-wide d half, all halves staged at once (no read wait in between)
+  static constexpr uint32_t kStageWarp = 4096 * kHalves;
   static constexpr uint32_t kStageHalf = 4 * kStageWarp;
   static constexpr uint32_t kOffStage = kOffV + kVStages * kTile;
   static constexpr uint32_t kOffBar = kOffStage + 2 * kStageHalf;
@@ -151,8 +144,8 @@ constexpr int kItemRing = PATTN_K1_ITEM_RING;
 
 struct Bars {
   uint64_t q_full, q_empty;
-  uint64_t k_full[kMaxStages], k_empty[kMaxStages];
-  uint64_t v_full[kMaxStages], v_empty[kMaxStages];
+  uint64_t k_full[kKStages], k_empty[kKStages];
+  uint64_t v_full[kVStages], v_empty[kVStages];
   uint64_t s_full[2][2], p_full[2], pv_done[2], o_empty[2];
   // dynamic work queue (see ItemSlot)
   uint64_t item_full[kItemRing], item_empty[kItemRing];
@@ -178,7 +171,6 @@ struct ItemSlot {
 constexpr uint32_t kOffItems = sizeof(Bars);
 static_assert(sizeof(Bars) + kItemRing * sizeof(ItemSlot) <= kBarBlock, "barrier block");
 
-template <int N>
 __device__ __forceinline__ Item prefill_item(const Params& p, int total_qb, int it, int lane) {
   Item x;
   const int j = total_qb - 1 - it / p.Hkv;  // last Q blocks (longest key range) first
@@ -192,7 +184,7 @@ __device__ __forceinline__ Item prefill_item(const Params& p, int total_qb, int 
   x.tok0 = qblk * p.block_q;
   x.ntok = min(p.block_q, x.qlen - x.tok0);
   x.kv_end = x.ctx + x.tok0 + x.ntok;  // keys visible to the Q block's last row
-  x.ntiles = (x.kv_end + N - 1) / N;
+  x.ntiles = (x.kv_end + kN - 1) / kN;
   return x;
 }
 
@@ -229,13 +221,11 @@ PATTN_DEVICE Item next_item(Bars& bar, const ItemSlot* ring, uint32_t n, int lan
   return x;
 }
 
-template <int D, typename E, int N>
+template <int D, typename E>
 __global__ void __launch_bounds__(kThreads, 1)
     k1_prefill(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmO,
                const __grid_constant__ KvHeadMaps maps, Params p) {
-  using Sh = K1Shape<D, N>;
-  constexpr int kN = N, kKStages = Sh::kKStages, kVStages = Sh::kVStages;
-  constexpr bool kPP = Sh::kPP;
+  using Sh = K1Shape<D>;
   constexpr uint32_t kOffQ = Sh::kOffQ, kOffK = Sh::kOffK, kOffV = Sh::kOffV, kOffStage = Sh::kOffStage,
                      kOffBar = Sh::kOffBar, kQTile = Sh::kQTile, kHalf = Sh::kHalf, kTile = Sh::kTile,
                      kSub16Bytes = Sh::kSub16Bytes, kStageWarp = Sh::kStageWarp, kGroup = Sh::kGroup;
@@ -338,7 +328,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint64_t* fullb = kv ? &bar.v_full[s] : &bar.k_full[s];
         uint64_t* emptyb = kv ? &bar.v_empty[s] : &bar.k_empty[s];
         uint8_t* base = smem + (kv ? kOffV : kOffK) + s * kTile;
-        const int i = i_lo + (lane % (kN / 32));
+        const int i = i_lo + (lane & 1);
         const int blk = __shfl_sync(0xffffffffu, id_cur, i);
         if (lane == 0) {
           if (owner) PATTN_K1_TRACE(24 + kv);
@@ -384,62 +374,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&bar.q_full, ic & 1u);
       if (leader) PATTN_K1_TRACE(41);
       tc_fence_after();
-      if constexpr (kPP) {
-        // Ping-pong schedule (128-key tiles, one S buffer per half): S_h(0); then per tile j:
-        // PV_h(j) as soon as P_h(j) is in TMEM, immediately followed by S_h(j+1) into the same
-        // columns (tcgen05 ops execute in issue order, so S_h(j+1) overwrites P_h(j) only after
-        // PV_h(j) read it).  The commit of s_full after S_h(j+1) also covers PV_h(j): when the
-        // softmax sees S_h(j+1), O_h is quiescent (PV_h(j) done, PV_h(j+1) not yet issued) and
-        // can be rescaled in place without a separate PV wait.
-        const int h = h_lo;
-        const uint32_t tS = tmem + kTmemS + 128 * h, tO = tmem + kTmemO + 128 * h;
-        const uint64_t dq = dQ + ((h * kQTile) >> 4);
-        auto issue_s = [&](int jt) {
-          const uint32_t ks = kc % kKStages;
-          mbar_wait(&bar.k_full[ks], (kc / kKStages) & 1u);
-          if (leader) PATTN_K1_TRACE(1);
-          tc_fence_after();
-          if (leader) {
-            const uint64_t dk = dK + ((ks * kTile) >> 4);
-#pragma unroll
-            for (int k = 0; k < D / 16; ++k) {
-              const uint32_t offq = ((k >> 2) * kHalf + (k & 3) * 32) >> 4;
-              const uint32_t offk = ((k >> 2) * 1024 + (k & 3) * 32) >> 4;
-              tc_mma_f16_ss(tS, dq + offq, dk + offk, idS, k > 0 ? 1u : 0u);
-            }
-            PATTN_K1_TRACE(7 + h);
-            tc_commit(&bar.s_full[h][0]);
-            tc_commit(&bar.k_empty[ks]);
-            if (jt == x.ntiles - 1) tc_commit(&bar.q_empty);
-          }
-          __syncwarp();
-          ++kc;
-        };
-        issue_s(0);
-        for (int jt = 0; jt < x.ntiles; ++jt) {
-          mbar_wait(&bar.p_full[h], pcnt & 1u);
-          if (leader) PATTN_K1_TRACE(3 + h);
-          if (jt == 0) mbar_wait(&bar.o_empty[h], (ic & 1u) ^ 1u);
-          const uint32_t vs = vc % kVStages;
-          mbar_wait(&bar.v_full[vs], (vc / kVStages) & 1u);
-          if (leader) PATTN_K1_TRACE(2);
-          tc_fence_after();
-          if (leader) {
-            const uint64_t dv = dV + ((vs * kTile) >> 4);
-#pragma unroll
-            for (int k = 0; k < kN / 16; ++k)
-              tc_mma_f16_ts(tO, tS + 8 * k, dv + ((k * kSub16Bytes) >> 4), idPV, (jt > 0 || k > 0) ? 1u : 0u);
-            PATTN_K1_TRACE(5 + h);
-            tc_commit(&bar.v_empty[vs]);
-            if (jt == x.ntiles - 1) tc_commit(&bar.pv_done[h]);
-          }
-          __syncwarp();
-          ++pcnt;
-          ++vc;
-          if (jt + 1 < x.ntiles) issue_s(jt + 1);
-        }
-        continue;
-      }
       // Iteration jt: S_a(jt), S_b(jt) into S buffer jt&1 of each half, then PV_a(jt-1),
       // PV_b(jt-1) from buffer (jt-1)&1.  S_h(jt) overwrites P_h(jt-2), whose PV was issued
       // one iteration earlier (tcgen05 ops execute in issue order), so the softmax of tile
@@ -513,7 +447,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         it = __shfl_sync(0xffffffffu, it, 0);
         volatile ItemSlot* e = ring + slot;
         if (it < n_items) {
-          const Item x = prefill_item<N>(p, total_qb, it, lane);
+          const Item x = prefill_item(p, total_qb, it, lane);
           const int nsb_valid = (x.kv_end + 15) / 16;
           const int id = (lane < 8 && lane < nsb_valid) ? __ldg(p.block_table + (int64_t)x.b * p.bt_stride + lane / n16)
                                                         : p.num_blocks;
@@ -592,7 +526,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       float m_run = -INFINITY, l_run = 0.f;
       float s[kN];
       for (int jt = 0; jt < x.ntiles; ++jt) {
-        const int sb = kPP ? 0 : (jt & 1);  // S buffer of this tile (P is written back over it)
+        const int sb = jt & 1;  // S buffer of this tile (P is written back over it)
         const uint32_t tS = tS0 + 64 * sb;
         mbar_wait(&bar.s_full[h][sb], (sb ? sc1 : sc0) & 1u);
         sc0 += sb ? 0u : 1u;
@@ -601,8 +535,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         {
           uint32_t* su = reinterpret_cast<uint32_t*>(s);
-#pragma unroll
-          for (int c0 = 0; c0 < kN; c0 += 32) PATTN_TMEM_LD32(tS + c0, (su + c0));
+          PATTN_TMEM_LD32(tS + 0, (su + 0));
+          PATTN_TMEM_LD32(tS + 32, (su + 32));
           tmem_wait_ld();
         }
         if (lead) PATTN_K1_TRACE(30 + h);
@@ -632,9 +566,30 @@ __global__ void __launch_bounds__(kThreads, 1)
           m_use = m_new;
         }
         const float nbase = m_use == -INFINITY ? 0.f : -m_use;
-        // O_h rescale in TMEM (tcgen05.ld/st are warp-collective (.sync.aligned): when ANY row
-        // of the warp needs it)
-        auto rescale_o = [&]() {
+        // packed fp32x2 FMA-pipe ops (FFMA2 / FADD2, sm_100): half the instructions for the
+        // exponent argument and the row sum
+        const uint64_t ca2 = f32x2(ca, ca), nb2 = f32x2(nbase, nbase);
+        uint64_t rs2[4] = {0ull, 0ull, 0ull, 0ull};
+        uint32_t pk[kN / 2];
+#pragma unroll
+        for (int c = 0; c < kN; c += 2) {
+          // e^{scale*qk - m} in the log2 domain
+          const uint64_t xx = ffma2(f32x2(s[c], s[c + 1]), ca2, nb2);
+          const float e0 = fast_exp2(f32x2_lo(xx)), e1 = fast_exp2(f32x2_hi(xx));
+          rs2[(c >> 1) & 3] = fadd2(rs2[(c >> 1) & 3], f32x2(e0, e1));
+          pk[c >> 1] = E::pack(e0, e1);
+        }
+        const uint64_t r01 = fadd2(rs2[0], rs2[1]), r23 = fadd2(rs2[2], rs2[3]), rr = fadd2(r01, r23);
+        const float rs = f32x2_lo(rr) + f32x2_hi(rr);
+        if (lead) PATTN_K1_TRACE(34 + h);
+        // O_h: PV_h(jt-1) (issued once P_h(jt-1) arrived, while this tile's exponentials ran)
+        // must be complete before O_h is corrected and before P_h(jt) can be consumed.
+        // (the wait cannot be skipped when no row rescales: mbarrier parity only tells phases
+        // apart one step back, so every pv_done phase must be observed in order)
+        if (jt > 0) {
+          mbar_wait(&bar.pv_done[h], (tc - 1) & 1u);
+          tc_fence_after();
+          // tcgen05.ld/st are warp-collective (.sync.aligned): rescale when ANY row of the warp needs it
           if (__any_sync(0xffffffffu, alpha != 1.f)) {
 #pragma unroll
             for (int c0 = 0; c0 < D; c0 += 32) {
@@ -646,53 +601,11 @@ __global__ void __launch_bounds__(kThreads, 1)
               PATTN_TMEM_ST32(tO + c0, o);
             }
           }
-        };
-        // ping-pong: S_h(jt) was issued after PV_h(jt-1), so O_h is already quiescent
-        if (kPP && jt > 0) rescale_o();
-        // packed fp32x2 FMA-pipe ops (FFMA2 / FADD2, sm_100): half the instructions for the
-        // exponent argument and the row sum; P (bf16, 2 per column) over the first kN/2
-        // columns of the S buffer (the A operand of PV_h), stored 64 keys at a time
-        const uint64_t ca2 = f32x2(ca, ca), nb2 = f32x2(nbase, nbase);
-        uint64_t rs2[4] = {0ull, 0ull, 0ull, 0ull};
-#pragma unroll
-        for (int c0 = 0; c0 < kN; c0 += 64) {
-          uint32_t pk[32];
-#pragma unroll
-          for (int c = 0; c < 64; c += 2) {
-            // e^{scale*qk - m} in the log2 domain
-            const uint64_t xx = ffma2(f32x2(s[c0 + c], s[c0 + c + 1]), ca2, nb2);
-            float e0, e1;
-            if (((c >> 1) & 7) < kPolyPairs) {  // FMA-pipe exponential for kPolyPairs of every 8 pairs
-              const uint64_t e = exp2_poly2(xx);
-              e0 = f32x2_lo(e);
-              e1 = f32x2_hi(e);
-            } else {
-              e0 = fast_exp2(f32x2_lo(xx));
-              e1 = fast_exp2(f32x2_hi(xx));
-            }
-            rs2[(c >> 1) & 3] = fadd2(rs2[(c >> 1) & 3], f32x2(e0, e1));
-            pk[c >> 1] = E::pack(e0, e1);
-          }
-          if (kPP || c0 + 64 == kN) {
-            if constexpr (!kPP) {
-              // O_h: PV_h(jt-1) (issued once P_h(jt-1) arrived, while this tile's exponentials
-              // ran) must be complete before O_h is corrected and before P_h(jt) can be consumed.
-              // (the wait cannot be skipped when no row rescales: mbarrier parity only tells
-              // phases apart one step back, so every pv_done phase must be observed in order)
-              if (jt > 0) {
-                mbar_wait(&bar.pv_done[h], (tc - 1) & 1u);
-                tc_fence_after();
-                rescale_o();
-              }
-            }
-            PATTN_TMEM_ST32(tS + c0 / 2, pk);
-          }
         }
-        const uint64_t r01 = fadd2(rs2[0], rs2[1]), r23 = fadd2(rs2[2], rs2[3]), rr = fadd2(r01, r23);
-        const float rs = f32x2_lo(rr) + f32x2_hi(rr);
-        if (lead) PATTN_K1_TRACE(34 + h);
         l_run = l_run * alpha + rs;
         m_run = m_use;
+        // P (bf16, 2 per column) over the first 32 columns of the S buffer: the A operand of PV_h
+        PATTN_TMEM_ST32(tS + 0, (pk + 0));
         // Zero V rows of slots >= L inside the last fetched sub-block (they may hold NaN); each
         // warpgroup does it before releasing its own P (both write the same zeros).
         {
@@ -718,8 +631,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ++tc;
       }
       // ---- epilogue: O / l -> bf16 -> out (valid rows only)
-      // (64-key tiles: one pv_done phase per tile; ping-pong: one per item)
-      mbar_wait(&bar.pv_done[h], kPP ? (ic & 1u) : ((tc - 1) & 1u));
+      mbar_wait(&bar.pv_done[h], (tc - 1) & 1u);
       if (lead) PATTN_K1_TRACE(42 + h);
       tc_fence_after();
       // this warp's O columns in one go, then O_h is released to the next item's PV_h(0)
@@ -748,11 +660,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int tok_w = x.q0 + x.tok0 + h * bq_half + (r & ~31) / G;
 #pragma unroll
         for (int pass = 0; pass < Sh::kHalves; ++pass) {
-          uint8_t* stg = stg0 + (pass % Sh::kStagePasses) * 4096;
-          if (pass >= Sh::kStagePasses) {  // slice reused within the item: its previous store has read it
-            if (lane == 0) bulk_wait_group_read0();
-            __syncwarp();
-          }
+          uint8_t* stg = stg0 + pass * 4096;
 #pragma unroll
           for (int c = 0; c < 8; ++c) {
             const int c0 = pass * 64 + c * 8;
@@ -815,31 +723,20 @@ bool prefill_supported(const Params& p) {
 
 int prefill_block_q(int G) { return 2 * (kHalfM / G); }
 
-PrefillLaunch plan_prefill(const Params& p, int num_sms, int tile_n) {
+PrefillLaunch plan_prefill(const Params& p, int num_sms) {
   PrefillLaunch pl;
   pl.grid = num_sms;
-  pl.tile_n = tile_n == 128 ? 128 : 64;
-  if (pl.tile_n == 128)
-    pl.smem = p.D == 64 ? K1Shape<64, 128>::kSmemBytes : K1Shape<128, 128>::kSmemBytes;
-  else
-    pl.smem = p.D == 64 ? K1Shape<64, 64>::kSmemBytes : K1Shape<128, 64>::kSmemBytes;
+  pl.smem = p.D == 64 ? K1Shape<64>::kSmemBytes : K1Shape<128>::kSmemBytes;
   return pl;
-}
-
-template <int N>
-static cudaError_t launch_prefill_n(const Params& p, const PrefillLaunch& pl, const CUtensorMap& tmQ,
-                                    const CUtensorMap& tmO, const KvHeadMaps& kv, cudaStream_t stream) {
-  auto kern = p.dtype == 2 ? (p.D == 64 ? k1_prefill<64, EltF16, N> : k1_prefill<128, EltF16, N>)
-                           : (p.D == 64 ? k1_prefill<64, EltBf16, N> : k1_prefill<128, EltBf16, N>);
-  cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(kern), pl.smem);
-  if (e != cudaSuccess) return e;
-  return launch_pdl(kern, dim3(pl.grid), dim3(kThreads), pl.smem, stream, tmQ, tmO, kv, p);
 }
 
 cudaError_t launch_prefill(const Params& p, const PrefillLaunch& pl, const CUtensorMap& tmQ, const CUtensorMap& tmO,
                            const KvHeadMaps& kv, cudaStream_t stream) {
-  return pl.tile_n == 128 ? launch_prefill_n<128>(p, pl, tmQ, tmO, kv, stream)
-                          : launch_prefill_n<64>(p, pl, tmQ, tmO, kv, stream);
+  auto kern = p.dtype == 2 ? (p.D == 64 ? k1_prefill<64, EltF16> : k1_prefill<128, EltF16>)
+                           : (p.D == 64 ? k1_prefill<64, EltBf16> : k1_prefill<128, EltBf16>);
+  cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(kern), pl.smem);
+  if (e != cudaSuccess) return e;
+  return launch_pdl(kern, dim3(pl.grid), dim3(kThreads), pl.smem, stream, tmQ, tmO, kv, p);
 }
 
 }  // namespace pattn

@@ -70,12 +70,11 @@ struct KvHeadMaps {
 };
 struct PrefillLaunch {
   int grid;
-  int tile_n;  // keys per KV tile: 64 (double-buffered S) or 128 (ping-pong schedule)
   size_t smem;
 };
 bool prefill_supported(const Params& p);
 int prefill_block_q(int G);  // tokens per K1 Q block (BLOCK_M / G)
-PrefillLaunch plan_prefill(const Params& p, int num_sms, int tile_n);
+PrefillLaunch plan_prefill(const Params& p, int num_sms);
 cudaError_t launch_prefill(const Params& p, const PrefillLaunch& pl, const CUtensorMap& tmQ, const CUtensorMap& tmO,
                            const KvHeadMaps& kv, cudaStream_t stream);
 

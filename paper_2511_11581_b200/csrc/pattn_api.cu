@@ -337,7 +337,7 @@ pattn_status_t make_plan(const pattn_problem_t* p, const void* q, const void* kc
   }
   fill_params(p, *pl, &probe);
   if (pl->use_k2) pl->dl = plan_decode(probe, pl->num_sms, pl->max_smem, pl->tuning.decode_ctas_per_sm);
-  if (pl->use_k1) pl->pl = plan_prefill(probe, pl->num_sms, env_int("PATTN_K1_TILE", 64));
+  if (pl->use_k1) pl->pl = plan_prefill(probe, pl->num_sms);
   return PATTN_OK;
 }
 
