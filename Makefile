@@ -8,7 +8,7 @@ LIBDIR  := paper_2511_11581_b200/lib
 NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC,-fvisibility=hidden -Xptxas -v \
            --expt-relaxed-constexpr -Iinclude -I$(CSRC) -DPATTN_BUILD $(EXTRA)
 SRCS    := $(CSRC)/pattn_api.cu $(CSRC)/k5_metadata.cu $(CSRC)/k4_generic.cu $(CSRC)/k2_decode.cu \
-           $(CSRC)/k3_reduce.cu $(CSRC)/k1_prefill.cu \
+           $(CSRC)/k3_reduce.cu $(CSRC)/k1_prefill.cu $(CSRC)/k2w_decode.cu \
            $(CSRC)/k6_write_kv.cu $(CSRC)/k7_baseline.cu
 OBJS    := $(patsubst $(CSRC)/%.cu,build/%.o,$(SRCS))
 HDRS    := $(wildcard $(CSRC)/*.h $(CSRC)/*.cuh) include/pattn.h

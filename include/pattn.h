@@ -128,7 +128,7 @@ typedef struct pattn_problem {
 enum {
   PATTN_KERNEL_METADATA = 0, /* K5: batch metadata + work lists */
   PATTN_KERNEL_PREFILL = 1,  /* K1: tcgen05/TMEM Q-block kernel */
-  PATTN_KERNEL_DECODE = 2,   /* K2: split-KV decode, "parallel tiled softmax" */
+  PATTN_KERNEL_DECODE = 2,   /* K2 / K2W: split-KV decode, "parallel tiled softmax" */
   PATTN_KERNEL_REDUCE = 3,   /* K3: segment reduction */
   PATTN_KERNEL_GENERIC = 4,  /* K4: generic SIMT Q-block kernel (fp32 path, fallback shapes) */
   PATTN_KERNEL_BASELINE = 5, /* K7: the paper's baseline kernel (PATTN_FLAG_BASELINE only) */
@@ -232,7 +232,7 @@ typedef struct pattn_tuning {
   int32_t decode_ctas_per_sm; /* decode: resident K2 CTAs per SM, 1..4 (default 2) */
   int32_t k2_sm_mbs;          /* mixed batches, two streams: decode streaming rate per SM (MB/s) that K5's
                                  SM-partition model assumes -- higher leaves more SMs to the prefill kernel
-                                 (default 61000) */
+                                 (default: the measured rate of the decode kernel in use, K2W 80000, K2 61000) */
   int32_t serial;             /* mixed batches: 1 = prefill and decode kernels back to back on one stream
                                  even when a second stream is given; 0 = concurrent (default) */
 } pattn_tuning_t;           /* 0 in a field = built-in default */
@@ -319,7 +319,10 @@ PATTN_API pattn_status_t pattn_debug_plan(const pattn_problem_t* p, const int32_
 /* Number of kernel launches pattn_unified_attention enqueues for this problem (host-side plan). */
 PATTN_API int32_t pattn_planned_launches(const pattn_problem_t* p);
 
-/* Bit mask of the kernel kinds (1 << PATTN_KERNEL_*) pattn_unified_attention launches for this problem. */
+/* Bit mask of the kernel kinds (1 << PATTN_KERNEL_*) pattn_unified_attention launches for this problem,
+ * plus PATTN_PLAN_DECODE_WIDE when the decode kind runs as K2W (head-wide TMA boxes, HB KV heads per
+ * work item; k2w_decode.cu) rather than K2. */
+#define PATTN_PLAN_DECODE_WIDE (1 << 8)
 PATTN_API int32_t pattn_planned_kernels(const pattn_problem_t* p);
 
 /* Text of the CUDA error behind the calling thread's last PATTN_ERR_CUDA ("" if none). */

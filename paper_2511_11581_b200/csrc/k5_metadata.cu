@@ -111,12 +111,35 @@ __global__ void __launch_bounds__(kMaxThreads) k5_metadata(Params p) {
     keys = block_sum_u64(my_keys, s_red);
   }
 
-  const long long units = p.k4_decodes ? (long long)p.Hkv : (long long)p.Hkv * p.HG;  // items per segment
+  // SM partition for concurrent K1 / K2: P minimising max(prefill time on P SMs, decode
+  // time on the other SMs, capped by HBM), from per-SM rates of the two kernels.
+  int P = p.num_sms;
+  if (p.partition) {
+    if (p.prefill_ctas_fixed > 0) {
+      P = min(p.prefill_ctas_fixed, p.num_sms);
+    } else if (tiles > 0 && keys > 0) {
+      // prefill time tp / c on c SMs; decode time bytes / min((S - c) b, HBM).  Balance
+      // point c* = S tp b / (tp b + bytes); below c_hbm = S - HBM / b the decode side is
+      // HBM-bound anyway, so P = max(c*, c_hbm).
+      const float S = (float)p.num_sms;
+      const float tp = (float)tiles * (float)p.Hkv * p.k1_tile_us * 1e-6f;  // SM-s
+      const float bytes = (float)keys * (float)p.Hkv * (float)p.D * 4.0f;   // K + V bf16
+      const float b = p.k2_sm_gbs * 1e9f;                                   // B/s per SM
+      const float cstar = S * tp * b / (tp * b + bytes);
+      const float chbm = S - p.hbm_gbs / p.k2_sm_gbs;
+      P = (int)(fmaxf(cstar, chbm) + 0.5f);
+      P = max(1, min(P, p.num_sms - 1));
+    }
+  }
+  const long long target = p.target_items;
+  const long long units = p.k4_decodes    ? (long long)p.Hkv
+                          : p.decode_hb ? (long long)(p.Hkv / p.decode_hb)
+                                        : (long long)p.Hkv * p.HG;  // items per segment
   long long C;
   if (p.split_mode == 1) {
     C = INT_MAX;
   } else {
-    long long want = ((long long)dec_blocks * units + p.target_items - 1) / p.target_items;
+    long long want = ((long long)dec_blocks * units + target - 1) / target;
     C = want > p.min_chunk_blocks ? want : p.min_chunk_blocks;
     if (C < 1) C = 1;
   }
@@ -159,26 +182,6 @@ __global__ void __launch_bounds__(kMaxThreads) k5_metadata(Params p) {
     p.hdr[kHdrPrefillCounter] = 0;
     p.hdr[kHdrDecodeCounter] = 0;
     p.hdr[kHdrHintViolation] = n_viol ? 1 : 0;
-    // SM partition for concurrent K1 / K2: P minimising max(prefill time on P SMs, decode
-    // time on the other SMs, capped by HBM), from per-SM rates of the two kernels.
-    int P = p.num_sms;
-    if (p.partition) {
-      if (p.prefill_ctas_fixed > 0) {
-        P = min(p.prefill_ctas_fixed, p.num_sms);
-      } else if (tiles > 0 && keys > 0) {
-        // prefill time tp / c on c SMs; decode time bytes / min((S - c) b, HBM).  Balance
-        // point c* = S tp b / (tp b + bytes); below c_hbm = S - HBM / b the decode side is
-        // HBM-bound anyway, so P = max(c*, c_hbm).
-        const float S = (float)p.num_sms;
-        const float tp = (float)tiles * (float)p.Hkv * p.k1_tile_us * 1e-6f;  // SM-s
-        const float bytes = (float)keys * (float)p.Hkv * (float)p.D * 4.0f;   // K + V bf16
-        const float b = p.k2_sm_gbs * 1e9f;                                   // B/s per SM
-        const float cstar = S * tp * b / (tp * b + bytes);
-        const float chbm = S - p.hbm_gbs / p.k2_sm_gbs;
-        P = (int)(fmaxf(cstar, chbm) + 0.5f);
-        P = max(1, min(P, p.num_sms - 1));
-      }
-    }
     p.hdr[kHdrPrefillCtas] = P;
   }
 }

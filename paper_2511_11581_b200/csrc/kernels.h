@@ -56,6 +56,12 @@ DecodeLaunch plan_decode(const Params& p, int num_sms, size_t max_smem, int ctas
 cudaError_t launch_decode(const Params& p, const DecodeLaunch& dl, const CUtensorMap& tmK, const CUtensorMap& tmV,
                           cudaStream_t stream);
 
+// K2W: split-KV decode with head-wide TMA boxes (HB KV heads per request; k2w_decode.cu).
+int wide_decode_heads(int Hkv, int G);  // HB in {8, 4, 2}, or 0 when K2W does not apply
+DecodeLaunch plan_decode_wide(const Params& p, int num_sms, size_t max_smem);
+cudaError_t launch_decode_wide(const Params& p, const DecodeLaunch& dl, const CUtensorMap& tmK,
+                               const CUtensorMap& tmV, cudaStream_t stream);
+
 // K3: segment reduction (LSE merge of decode partials).
 cudaError_t launch_reduce(const Params& p, cudaStream_t stream);
 

@@ -159,7 +159,6 @@ pattn_tuning_t resolve_tuning(const pattn_problem_t* p) {
   if ((e = getenv("PATTN_DECODE_CTAS")) && *e) t.decode_ctas_per_sm = atoi(e);
   if ((e = getenv("PATTN_K2_SM_GBS")) && *e) t.k2_sm_mbs = (int32_t)(atof(e) * 1000.0);
   if ((e = getenv("PATTN_SERIAL")) && *e) t.serial = atoi(e) ? 1 : 0;
-  if (t.k2_sm_mbs <= 0) t.k2_sm_mbs = 61000;
   if (t.items_per_sm <= 0) t.items_per_sm = 16;
   if (t.min_chunk_tokens <= 0) t.min_chunk_tokens = 256;
   if (t.decode_ctas_per_sm <= 0) t.decode_ctas_per_sm = 2;
@@ -172,6 +171,7 @@ struct Plan {
   bool k4_decodes = false;  // decode segments on K4 (when K2 cannot take them)
   bool kv_vec16 = false;    // K/V rows 16-byte aligned (K4 vector loads)
   int block_q = 1, HG = 1, rpw = 8;
+  int decode_hb = 0;  // > 0: decodes on K2W (head-wide boxes)
   int target_items = 0, min_chunk = 1, split_mode = 0, max_chunks = 0;
   int num_sms = 148;
   size_t max_smem = 0;
@@ -214,6 +214,7 @@ void fill_params(const pattn_problem_t* p, const Plan& pl, Params* k) {
   k->dtype = p->dtype;
   k->block_q = pl.block_q;
   k->HG = pl.HG;
+  k->decode_hb = pl.decode_hb;
   k->max_chunks = pl.max_chunks;
   k->decode_split = (pl.use_k2 || pl.k4_decodes) ? 1 : 0;
   k->k4_decodes = pl.k4_decodes ? 1 : 0;
@@ -305,8 +306,18 @@ pattn_status_t make_plan(const pattn_problem_t* p, const void* q, const void* kc
   }
   if (pl->target_items < 1) pl->target_items = 1;
   if (pl->min_chunk < 1) pl->min_chunk = 1;
+  // K2W: decode items of HB KV heads (one TMA request per 16 keys x HB heads; default whenever
+  // G <= 8 and 2 | Hkv, PATTN_DECODE_WIDE=0 keeps K2).  Its items are HB x larger than K2's, so
+  // the segment plan targets fewer of them: 4 per SM (measured best of 4 / 8 / 16 on configs 2-5;
+  // more segments cost K3 partial traffic: config 4 at 32 per SM wrote 153 MB of partials).
+  if (pl->use_k2 && env_int("PATTN_DECODE_WIDE", 1)) pl->decode_hb = wide_decode_heads(p->num_kv_heads, G);
+  if (pl->decode_hb && !(p->flags & (PATTN_FLAG_NO_SPLIT | PATTN_FLAG_FORCE_SPLIT))) {
+    pl->target_items = std::max(1, env_int("PATTN_TARGET_ITEMS", pl->num_sms * env_int("PATTN_WIDE_ITEMS_PER_SM", 4)));
+  }
   const long long units = (long long)p->num_kv_heads * pl->HG;
-  const long long seg_units = pl->k4_decodes ? (long long)p->num_kv_heads : units;  // K4: all G heads per item
+  const long long seg_units = pl->k4_decodes  ? (long long)p->num_kv_heads  // K4: all G heads per item
+                              : pl->decode_hb ? (long long)(p->num_kv_heads / pl->decode_hb)
+                                              : units;
   pl->max_chunks = (pl->use_k2 || pl->k4_decodes)
                        ? (int)(p->num_seqs + (pl->target_items + seg_units - 1) / seg_units + 1)
                        : 0;
@@ -336,7 +347,9 @@ pattn_status_t make_plan(const pattn_problem_t* p, const void* q, const void* kc
     if (pl->k4_grid < 1) pl->k4_grid = 1;
   }
   fill_params(p, *pl, &probe);
-  if (pl->use_k2) pl->dl = plan_decode(probe, pl->num_sms, pl->max_smem, pl->tuning.decode_ctas_per_sm);
+  if (pl->use_k2)
+    pl->dl = pl->decode_hb ? plan_decode_wide(probe, pl->num_sms, pl->max_smem)
+                           : plan_decode(probe, pl->num_sms, pl->max_smem, pl->tuning.decode_ctas_per_sm);
   if (pl->use_k1) pl->pl = plan_prefill(probe, pl->num_sms);
   return PATTN_OK;
 }
@@ -404,7 +417,7 @@ bool encode_head_maps(KvHeadMaps* out, const pattn_problem_t* p, const void* kc,
 // the d-half dim, 128 B, sits outside the slot dim) so that ONE box {64, 16, D/64, 1, 1}
 // brings a whole 16-key sub-block of one head into shared memory as [half][slot][64 d],
 // the layout two 4-D boxes give -- half the TMA issues for the decode producer.
-bool encode_kv_map5(CUtensorMap* tm, const pattn_problem_t* p, const void* base) {
+bool encode_kv_map5(CUtensorMap* tm, const pattn_problem_t* p, const void* base, int box_heads = 1) {
   auto fn = encode_fn();
   if (!fn) return false;
   const int halves = p->head_dim / 64;
@@ -412,7 +425,7 @@ bool encode_kv_map5(CUtensorMap* tm, const pattn_problem_t* p, const void* base)
                         (cuuint64_t)p->num_blocks};
   cuuint64_t strides[4] = {(cuuint64_t)p->kv_stride_tok * 2, 128, (cuuint64_t)p->kv_stride_head * 2,
                            (cuuint64_t)p->kv_stride_blk * 2};
-  cuuint32_t box[5] = {64, 16, (cuuint32_t)halves, 1, 1};
+  cuuint32_t box[5] = {64, 16, (cuuint32_t)halves, (cuuint32_t)box_heads, 1};  // K2W: HB heads per box
   cuuint32_t estr[5] = {1, 1, 1, 1, 1};
   CUresult r = fn(tm, tma_dtype(p), 5, const_cast<void*>(base), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -534,7 +547,8 @@ pattn_status_t run(const pattn_problem_t* p, const void* q, const void* k_cache,
   static thread_local KvHeadMaps head_maps;  // 16 KB: kept off the stack
   if (!metadata_only) {
     if (pl.use_k2) {
-      if (!encode_kv_map5(&tmK5, p, k_cache) || !encode_kv_map5(&tmV5, p, v_cache)) return PATTN_ERR_UNSUPPORTED;
+      const int hb = pl.decode_hb > 0 ? pl.decode_hb : 1;
+      if (!encode_kv_map5(&tmK5, p, k_cache, hb) || !encode_kv_map5(&tmV5, p, v_cache, hb)) return PATTN_ERR_UNSUPPORTED;
     }
     if (pl.use_k1) {
       if (!encode_head_maps(&head_maps, p, k_cache, v_cache)) return PATTN_ERR_UNSUPPORTED;
@@ -552,7 +566,11 @@ pattn_status_t run(const pattn_problem_t* p, const void* q, const void* k_cache,
     k.partition = 1;
     k.prefill_ctas_fixed = env_int("PATTN_PREFILL_SMS", 0);
     k.k1_tile_us = env_float("PATTN_K1_TILE_US", 2.8f);
-    k.k2_sm_gbs = (float)pl.tuning.k2_sm_mbs * 1e-3f;
+    // per-SM decode rate of the partition model: the tree / env value, else the measured
+    // default of the decode kernel in use (K2W: PATTN_K2W_SM_GBS, K2: 61 GB/s/SM)
+    k.k2_sm_gbs = pl.tuning.k2_sm_mbs > 0 ? (float)pl.tuning.k2_sm_mbs * 1e-3f
+                  : pl.decode_hb          ? env_float("PATTN_K2W_SM_GBS", 80.f)
+                                          : 61.f;
     k.hbm_gbs = env_float("PATTN_HBM_GBS", 6300.f);
   }
 
@@ -587,7 +605,9 @@ pattn_status_t run(const pattn_problem_t* p, const void* q, const void* k_cache,
   };
   if (pl.use_k1) step(PATTN_KERNEL_PREFILL, s1, [&] { return launch_prefill(k, pl.pl, tmQ, tmO, head_maps, s1); });
   if (pl.use_k2) {
-    step(PATTN_KERNEL_DECODE, sd, [&] { return launch_decode(k, pl.dl, tmK5, tmV5, sd); });
+    step(PATTN_KERNEL_DECODE, sd, [&] {
+      return pl.decode_hb ? launch_decode_wide(k, pl.dl, tmK5, tmV5, sd) : launch_decode(k, pl.dl, tmK5, tmV5, sd);
+    });
     step(PATTN_KERNEL_REDUCE, sd, [&] { return launch_reduce(k, sd); });
   }
   if (pl.use_k7) step(PATTN_KERNEL_BASELINE, s1, [&] { return launch_baseline(k, s1); });
@@ -787,7 +807,8 @@ int32_t pattn_planned_kernels(const pattn_problem_t* p) {
   return (1 << PATTN_KERNEL_METADATA) | (pl.use_k1 ? 1 << PATTN_KERNEL_PREFILL : 0) |
          (pl.use_k2 ? (1 << PATTN_KERNEL_DECODE) | (1 << PATTN_KERNEL_REDUCE) : 0) |
          (pl.k4_decodes ? (1 << PATTN_KERNEL_REDUCE) : 0) |
-         (pl.use_k4 ? 1 << PATTN_KERNEL_GENERIC : 0) | (pl.use_k7 ? 1 << PATTN_KERNEL_BASELINE : 0);
+         (pl.use_k4 ? 1 << PATTN_KERNEL_GENERIC : 0) | (pl.use_k7 ? 1 << PATTN_KERNEL_BASELINE : 0) |
+         (pl.decode_hb ? PATTN_PLAN_DECODE_WIDE : 0);
 }
 
 pattn_status_t pattn_write_kv(const pattn_problem_t* p, const void* k_new, const void* v_new,

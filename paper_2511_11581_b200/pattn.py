@@ -35,6 +35,7 @@ DTYPE_F32, DTYPE_BF16, DTYPE_F16 = 0, 1, 2
 FLAG_FORCE_GENERIC, FLAG_NO_SPLIT, FLAG_FORCE_SPLIT, FLAG_SERIAL, FLAG_BASELINE = 0x1, 0x2, 0x4, 0x8, 0x10
 KERNEL_METADATA, KERNEL_PREFILL, KERNEL_DECODE, KERNEL_REDUCE, KERNEL_GENERIC, KERNEL_BASELINE, KERNEL_COUNT = range(7)
 KERNEL_NAMES = ["metadata", "prefill", "decode", "reduce", "generic", "baseline"]
+PLAN_DECODE_WIDE = 1 << 8  # planned_kernels(): the decode kind runs as K2W (head-wide TMA boxes)
 
 
 class PattnError(RuntimeError):

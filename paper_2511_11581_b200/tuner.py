@@ -35,7 +35,8 @@ KNOBS = ["items_per_sm", "min_chunk_tokens", "decode_ctas_per_sm", "k2_sm_mbs", 
 
 
 # libpattn's built-in value of each knob (used where a tree leaf or record holds 0)
-DEFAULTS = {"items_per_sm": 16, "min_chunk_tokens": 256, "decode_ctas_per_sm": 2, "k2_sm_mbs": 61000, "serial": 0}
+# k2_sm_mbs 0: the measured per-SM rate of the decode kernel the planner picks (K2W 80 GB/s, K2 61 GB/s)
+DEFAULTS = {"items_per_sm": 16, "min_chunk_tokens": 256, "decode_ctas_per_sm": 2, "k2_sm_mbs": 0, "serial": 0}
 
 
 def with_defaults(cfg: Dict) -> Dict:

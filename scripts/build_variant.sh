@@ -8,7 +8,7 @@ cd "$(dirname "$0")/.."
 SRC=${SRC:-paper_2511_11581_b200/csrc}
 mkdir -p variants/$name/build
 objs=""
-for f in pattn_api k5_metadata k4_generic k2_decode k3_reduce k1_prefill k6_write_kv k7_baseline; do
+for f in pattn_api k5_metadata k4_generic k2_decode k2w_decode k3_reduce k1_prefill k6_write_kv k7_baseline; do
   /usr/local/cuda/bin/nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo \
     -Xcompiler -fPIC,-fvisibility=hidden --expt-relaxed-constexpr -Iinclude -I$SRC \
     -DPATTN_BUILD "$@" -c $SRC/$f.cu -o variants/$name/build/$f.o &

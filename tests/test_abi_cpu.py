@@ -88,8 +88,16 @@ def test_workspace_and_planned_launches(lib, monkeypatch):
     pb = _problem(lib, Hq=32, Hkv=8, D=128, dtype=1, T=64, B=64, nb=16448, maxb=257)
     pb.max_query_len = 1
     assert lib.planned_launches(pb) == 3  # metadata + decode + reduce
+    # G = 4, Hkv = 8: the decode kind runs as K2W (8 KV heads per TMA box)
+    assert lib.planned_kernels(pb) == (1 << lib.KERNEL_METADATA) | (1 << lib.KERNEL_DECODE) | (
+        1 << lib.KERNEL_REDUCE) | lib.PLAN_DECODE_WIDE
+    monkeypatch.setenv("PATTN_DECODE_WIDE", "0")  # K2 (one KV head per item)
     assert lib.planned_kernels(pb) == (1 << lib.KERNEL_METADATA) | (1 << lib.KERNEL_DECODE) | (
         1 << lib.KERNEL_REDUCE)
+    monkeypatch.delenv("PATTN_DECODE_WIDE")
+    pg = _problem(lib, Hq=64, Hkv=4, D=128, dtype=1, T=64, B=64, nb=16448, maxb=257)  # G = 16: K2
+    pg.max_query_len = 1
+    assert not lib.planned_kernels(pg) & lib.PLAN_DECODE_WIDE
     pb.max_query_len = 2048
     assert lib.planned_launches(pb) == 4  # + the Q-block kernel
     pb.flags = lib.FLAG_FORCE_GENERIC

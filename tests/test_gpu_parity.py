@@ -347,6 +347,8 @@ def test_compute_sanitizer_memcheck_and_racecheck():
     for tool, seqs in (("memcheck", "6x3000:1+2x0:300+1x50:70"), ("racecheck", "2x700:1+1x0:200"), ("synccheck", "2x700:1+1x0:200")):
         r = subprocess.run([exe, "--tool", tool, "--error-exitcode", "3", "python", script, "c3_mixed8b", "1", seqs],
                            capture_output=True, text=True, timeout=900)
+        if "ERROR SUMMARY" not in r.stdout and "closed on this pool" in (r.stdout + r.stderr):
+            pytest.skip("compute-sanitizer is disabled on this GPU pool")
         # the only accepted report is torch's own benign cuKernelGetFunction probe
         errs = [l for l in r.stdout.splitlines() if "ERROR SUMMARY" in l]
         assert r.returncode in (0, 3), r.stdout[-2000:] + r.stderr[-2000:]
@@ -631,3 +633,61 @@ def test_shape_fuzz(i):
                         decode_share=float(rng.uniform(0.2, 0.8)))
     batch = generate(w, seed=i, dist="peaked", layout=layout, poison=True)
     _check(batch, 0, f"fuzz {i}: heads {heads} D{D} bs{bs} {dt} {layout} {w.seqs}")
+
+
+# ---------------------------------------------------------------- decode kernels K2 and K2W
+# K2W (head-wide TMA boxes, HB KV heads per item) is the default decode kernel when G <= 8 and
+# 2 | Hkv; K2 (one KV head per item) stays for the rest and under PATTN_DECODE_WIDE=0.  Both are
+# checked against the oracle on the same batches, for every HB K2W instantiates (PATTN_DECODE_WIDE_HB
+# caps it), and the plan is checked to route where it says.
+DECODE_CASES = [
+    # heads, D, bs, dtype, layout
+    ((32, 8), 128, 16, "bf16", "NHD"),
+    ((64, 8), 128, 32, "bf16", "HND"),
+    ((28, 4), 128, 16, "bf16", "NHD"),   # G = 7
+    ((16, 2), 64, 48, "bf16", "NHD"),    # G = 8, D = 64, HB = 2
+    ((32, 8), 64, 16, "f16", "HND"),
+    ((12, 6), 128, 16, "bf16", "NHD"),   # Hkv = 6 -> HB = 2
+]
+
+
+@pytest.mark.parametrize("case", range(len(DECODE_CASES)))
+@pytest.mark.parametrize("hb_cap", [8, 4, 2, 0])
+def test_decode_wide_and_narrow(case, hb_cap, monkeypatch):
+    heads, D, bs, dt, layout = DECODE_CASES[case]
+    rng = np.random.default_rng(700 + case)
+    seqs = [(int(rng.integers(1, 6000)), 1) for _ in range(9)] + [(int(rng.integers(0, 300)), int(rng.integers(2, 40)))]
+    w = Workload(f"dec{case}", tuple(seqs), heads[0], heads[1], D, bs, dt)
+    batch = generate(w, seed=case, dist="peaked", layout=layout, poison=True)
+    if hb_cap == 0:
+        monkeypatch.setenv("PATTN_DECODE_WIDE", "0")
+    else:
+        monkeypatch.setenv("PATTN_DECODE_WIDE_HB", str(hb_cap))
+    db = DeviceBatch(batch)
+    prob = P.make_problem(db.q, db.k, w.num_kv_heads, w.block_size, db.bt, w.num_seqs, kv_layout=layout)
+    wide = bool(P.planned_kernels(prob) & P.PLAN_DECODE_WIDE)
+    assert wide == (hb_cap > 0 and heads[0] // heads[1] <= 8), (heads, hb_cap, wide)
+    ref = O.batch_attention(batch)
+    for flags in (0, P.FLAG_FORCE_SPLIT, P.FLAG_NO_SPLIT):
+        assert_close(out_f64(db.run(flags=flags)), ref, dt, f"{w.name} hb<={hb_cap} flags={flags}")
+
+
+def test_decode_wide_equals_narrow_needles(monkeypatch):
+    """Needle rows through both decode kernels: bit-exact V rows (one dominant key per KV head)."""
+    w = Workload("wneedle", tuple([(3000 + 7 * i, 1) for i in range(6)]), 32, 8, 128, 16, "bf16")
+    batch = generate(w, seed=77, dist="needle")
+    v = O.widen(batch.v_cache)
+    outs = []
+    for wide in ("1", "0"):
+        monkeypatch.setenv("PATTN_DECODE_WIDE", wide)
+        out = DeviceBatch(batch).run(flags=P.FLAG_FORCE_SPLIT).cpu()
+        for b in range(w.num_seqs):
+            s = int(batch.cu_seqlens_q[b])
+            for g in range(w.num_kv_heads):
+                t = int(batch.needle_pos[b, g])
+                row = torch.from_numpy(v[batch.block_table[b, t // 16], t % 16, g]).to(torch.bfloat16)
+                for h in range(g * 4, g * 4 + 4):
+                    assert torch.equal(out[s, h], row), (wide, b, g, h, t)
+        outs.append(out)
+    assert torch.equal(outs[0], outs[1])
+

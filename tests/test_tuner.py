@@ -8,7 +8,7 @@ import pytest
 
 from paper_2511_11581_b200 import tuner
 
-A = {"items_per_sm": 16, "min_chunk_tokens": 256, "decode_ctas_per_sm": 2, "k2_sm_mbs": 61000, "serial": 0}
+A = {"items_per_sm": 16, "min_chunk_tokens": 256, "decode_ctas_per_sm": 2, "k2_sm_mbs": 0, "serial": 0}
 B = {"items_per_sm": 4, "min_chunk_tokens": 1024, "decode_ctas_per_sm": 3, "k2_sm_mbs": 80000, "serial": 0}
 C = {"items_per_sm": 32, "min_chunk_tokens": 64, "decode_ctas_per_sm": 1, "k2_sm_mbs": 45000, "serial": 1}
 
