@@ -35,6 +35,7 @@ namespace {
 
 constexpr int kSub = 16;       // keys per sub-block (one mma M tile)
 constexpr int kItemRing = 8;   // producer -> consumers item queue
+constexpr float kLazyMax = 8.f;  // log2 domain: rescale only when a score exceeds the running max by > 2^8
 
 template <int D, int HB>
 struct WideShape {
@@ -42,8 +43,7 @@ struct WideShape {
   static constexpr int kKC = D / 16;                     // k-chunks of S^T, m-tiles of O^T
   static constexpr int kHalfBytes = kSub * 128;          // [slot][64 d] of one d half
   static constexpr int kHeadBytes = kHalves * kHalfBytes;  // one head's 16 keys of K (or V)
-  static constexpr int kOpBytes = HB * kHeadBytes;       // one box: HB heads
-  static constexpr int kStageBytes = 2 * kOpBytes;       // K box + V box
+  static constexpr int kOpBytes = HB * kHeadBytes;       // one box (ring entry): HB heads of K or of V
 };
 
 struct WItem {
@@ -74,13 +74,16 @@ __device__ __forceinline__ WItem wide_item(const Params& p, int it, int ngroups)
 template <int D, int HB, typename E>
 __global__ void __launch_bounds__((HB + 1) * 32, 1)
     k2w_decode(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, Params p,
-               int nst) {
+               int nent) {
   using S = WideShape<D, HB>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(ring + (size_t)nst * S::kStageBytes);
-  uint64_t* empty = full + nst;
-  uint64_t* item_full = empty + nst;
+  // Ring of nent entries, each ONE operand box (K or V of a 16-key sub-block, HB heads): the
+  // producer fills K(j), V(j) into consecutive entries; the consumers release K(j) right after
+  // the scores, so the next boxes are in flight while PV(j) still reads V(j).
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + (size_t)nent * S::kOpBytes);
+  uint64_t* empty = full + nent;
+  uint64_t* item_full = empty + nent;
   uint64_t* item_empty = item_full + kItemRing;
   volatile int* item_ring = reinterpret_cast<volatile int*>(item_empty + kItemRing);
 
@@ -99,7 +102,7 @@ __global__ void __launch_bounds__((HB + 1) * 32, 1)
     if (s_leave) return;
   }
   if (threadIdx.x == 0) {
-    for (int s = 0; s < nst; ++s) {
+    for (int s = 0; s < nent; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], HB);
     }
@@ -122,7 +125,9 @@ __global__ void __launch_bounds__((HB + 1) * 32, 1)
       tma_prefetch_desc(&tmV);
     }
     const uint64_t policy = l2_policy_evict_first();  // K/V are streamed exactly once
-    uint32_t g = 0;                                   // CTA-global sub-block (stage) counter
+    // ring position of the next entry, kept incrementally (nent is a runtime value: g % nent
+    // and g / nent cost an integer division per entry on the consumers' critical path)
+    uint32_t s = 0, ph = 0;
     for (uint32_t ni = 0;; ++ni) {
       int it = 0;
       if (lane == 0) {
@@ -145,15 +150,16 @@ __global__ void __launch_bounds__((HB + 1) * 32, 1)
         for (int jj = 0; jj < n; ++jj) {
           const int blk = __shfl_sync(0xffffffffu, id, jj);
           if (lane == 0) {
-            const uint32_t s = g % nst;
-            mbar_wait(&empty[s], ((g / nst) & 1u) ^ 1u);
-            mbar_arrive_expect_tx(&full[s], S::kStageBytes);
-            uint8_t* st = ring + (size_t)s * S::kStageBytes;
             const int slot0 = ((j0 + jj) % n16) * kSub;
-            tma_load_5d_hint(st, &tmK, &full[s], 0, slot0, 0, x.hb * HB, blk, policy);
-            tma_load_5d_hint(st + S::kOpBytes, &tmV, &full[s], 0, slot0, 0, x.hb * HB, blk, policy);
+#pragma unroll
+            for (int op = 0; op < 2; ++op) {  // K, then V
+              mbar_wait(&empty[s], ph ^ 1u);
+              mbar_arrive_expect_tx(&full[s], S::kOpBytes);
+              tma_load_5d_hint(ring + (size_t)s * S::kOpBytes, op ? &tmV : &tmK, &full[s], 0, slot0, 0, x.hb * HB,
+                               blk, policy);
+              if (++s == (uint32_t)nent) s = 0, ph ^= 1u;
+            }
           }
-          ++g;
         }
       }
     }
@@ -169,7 +175,7 @@ __global__ void __launch_bounds__((HB + 1) * 32, 1)
   const ET* Q = static_cast<const ET*>(p.q);
   const uint32_t ring_u32 = smem_u32(ring);
   const int G = p.G;
-  uint32_t g = 0;
+  uint32_t s = 0, ph = 0;  // ring position of the next stage (incremental, as the producer)
   for (uint32_t ni = 0;; ++ni) {
     const uint32_t slot = ni % kItemRing;
     mbar_wait(&item_full[slot], (ni / kItemRing) & 1u);
@@ -197,12 +203,17 @@ __global__ void __launch_bounds__((HB + 1) * 32, 1)
     for (int t = 0; t < S::kKC; ++t) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0.f;
 
     const int nsb = x.sb1 - x.sb0;
-    for (int j = 0; j < nsb; ++j, ++g) {
-      const uint32_t s = g % nst;
-      mbar_wait(&full[s], (g / nst) & 1u);
-      const uint32_t kst = ring_u32 + s * S::kStageBytes + w * S::kHeadBytes;
-      const uint32_t vst = kst + S::kOpBytes;
-      float sc[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int j = 0; j < nsb; ++j) {
+      mbar_wait(&full[s], ph);  // K(j)
+      const uint32_t kst = ring_u32 + s * S::kOpBytes + w * S::kHeadBytes;
+      const uint32_t ks = s;
+      if (++s == (uint32_t)nent) s = 0, ph ^= 1u;
+      const uint32_t vs = s, vph = ph;  // V(j): the next entry
+      if (++s == (uint32_t)nent) s = 0, ph ^= 1u;
+      const uint32_t vst = ring_u32 + vs * S::kOpBytes + w * S::kHeadBytes;
+      // two independent accumulation chains (even / odd k-chunks), summed: half the
+      // dependent mma latency of one chain (HMMA issues at most every 8 clk per warp)
+      float sc[4] = {0.f, 0.f, 0.f, 0.f}, sd[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int kc = 0; kc < S::kKC; ++kc) {
         const int key = (mat & 1) * 8 + mrow;
@@ -210,12 +221,20 @@ __global__ void __launch_bounds__((HB + 1) * 32, 1)
         const uint32_t addr = kst + (dd >> 6) * S::kHalfBytes + key * 128 + ((((dd & 63) >> 3) ^ (key & 7)) << 4);
         uint32_t a0, a1, a2, a3;
         ldmatrix_x4(addr, a0, a1, a2, a3);
-        E::mma(sc, a0, a1, a2, a3, bq[kc][0], bq[kc][1]);
+        if (kc & 1)
+          E::mma(sd, a0, a1, a2, a3, bq[kc][0], bq[kc][1]);
+        else
+          E::mma(sc, a0, a1, a2, a3, bq[kc][0], bq[kc][1]);
       }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) sc[i] += sd[i];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[ks]);  // K(j) consumed (the ldmatrix results fed the mma)
+      mbar_wait(&full[vs], vph);
       const int valid = x.L - (x.sb0 + j) * kSub;  // slots [0, valid) hold real keys
       if (valid < kSub) {
         // zero this head's V rows past the sequence end (NaN * 0 = NaN inside the mma)
-        uint8_t* vgen = ring + (size_t)s * S::kStageBytes + S::kOpBytes + w * S::kHeadBytes;
+        uint8_t* vgen = ring + (size_t)vs * S::kOpBytes + w * S::kHeadBytes;
         const int nrow = kSub - valid;
         for (int e = lane; e < nrow * 8 * S::kHalves; e += 32) {
           const int h = e / (nrow * 8);
@@ -231,27 +250,37 @@ __global__ void __launch_bounds__((HB + 1) * 32, 1)
       const float s1 = r < valid ? sc[1] * p.scale_log2 : -INFINITY;
       const float s2 = r + 8 < valid ? sc[2] * p.scale_log2 : -INFINITY;
       const float s3 = r + 8 < valid ? sc[3] * p.scale_log2 : -INFINITY;
+      // Lazy running max (as K1): the exponentials use the running max m unless a score
+      // exceeds it by more than 2^8 (log2 domain) -- then, and on an item's first stage
+      // (m = -inf), the max is reduced over the 16 keys and O and l are rescaled.  Exact
+      // softmax either way (the reference point cancels in acc / l); p <= 2^8 otherwise.  This
+      // takes the cross-lane max, two exponentials and the accumulator rescale off the common
+      // per-stage path (the consumers are latency-bound: one stage per warp per ~1000 clk).
       float mt0 = fmaxf(s0, s2), mt1 = fmaxf(s1, s3);
+      if (__any_sync(0xffffffffu, mt0 > m0 + kLazyMax || mt1 > m1 + kLazyMax)) {
 #pragma unroll
-      for (int o = 4; o < 32; o <<= 1) {
-        mt0 = fmaxf(mt0, __shfl_xor_sync(0xffffffffu, mt0, o));
-        mt1 = fmaxf(mt1, __shfl_xor_sync(0xffffffffu, mt1, o));
-      }
-      const float mn0 = fmaxf(m0, mt0), mn1 = fmaxf(m1, mt1);  // finite: every sub-block has a valid key
-      const float al0 = fast_exp2(m0 - mn0), al1 = fast_exp2(m1 - mn1);
-      const float p0 = fast_exp2(s0 - mn0), p1 = fast_exp2(s1 - mn1);
-      const float p2 = fast_exp2(s2 - mn0), p3 = fast_exp2(s3 - mn1);
-      l0 = fmaf(l0, al0, p0 + p2);
-      l1 = fmaf(l1, al1, p1 + p3);
-      m0 = mn0;
-      m1 = mn1;
+        for (int o = 4; o < 32; o <<= 1) {
+          mt0 = fmaxf(mt0, __shfl_xor_sync(0xffffffffu, mt0, o));
+          mt1 = fmaxf(mt1, __shfl_xor_sync(0xffffffffu, mt1, o));
+        }
+        const float mn0 = fmaxf(m0, mt0), mn1 = fmaxf(m1, mt1);  // finite: every sub-block has a valid key
+        const float al0 = fast_exp2(m0 - mn0), al1 = fast_exp2(m1 - mn1);
+        l0 *= al0;
+        l1 *= al1;
+        m0 = mn0;
+        m1 = mn1;
 #pragma unroll
-      for (int t = 0; t < S::kKC; ++t) {
-        acc[t][0] *= al0;
-        acc[t][1] *= al1;
-        acc[t][2] *= al0;
-        acc[t][3] *= al1;
+        for (int t = 0; t < S::kKC; ++t) {
+          acc[t][0] *= al0;
+          acc[t][1] *= al1;
+          acc[t][2] *= al0;
+          acc[t][3] *= al1;
+        }
       }
+      const float p0 = fast_exp2(s0 - m0), p1 = fast_exp2(s1 - m1);
+      const float p2 = fast_exp2(s2 - m0), p3 = fast_exp2(s3 - m1);
+      l0 += p0 + p2;
+      l1 += p1 + p3;
       // P^T as the B operand of O^T = V^T . P^T (transpose the 8x8 halves in registers)
       const uint32_t pb0 = movmatrix_trans(E::pack(p0, p1));
       const uint32_t pb1 = movmatrix_trans(E::pack(p2, p3));
@@ -266,7 +295,7 @@ __global__ void __launch_bounds__((HB + 1) * 32, 1)
       }
       __syncwarp();
       if (valid < kSub) fence_proxy_async_smem();  // generic zero-writes before the next TMA fill
-      if (lane == 0) mbar_arrive(&empty[s]);
+      if (lane == 0) mbar_arrive(&empty[vs]);
     }
 
     // ---- this head's result: row sums over the 8 key rows, then output or partial
@@ -356,17 +385,17 @@ int wide_decode_heads(int Hkv, int G) {
 DecodeLaunch plan_decode_wide(const Params& p, int num_sms, size_t max_smem) {
   DecodeLaunch dl;
   dl.consumer_warps = p.decode_hb;
-  const size_t stage = (size_t)2 * kSub * p.decode_hb * p.D * 2;
+  const size_t entry = (size_t)kSub * p.decode_hb * p.D * 2;  // one operand box
   const size_t fixed = 1024 /*align slack*/ + 2 * kItemRing * sizeof(uint64_t) + kItemRing * sizeof(int) + 64;
   const size_t cap = (max_smem < 227 * 1024 ? max_smem : 227 * 1024);
   const char* e = getenv("PATTN_DECODE_RING_KB");
-  size_t want = (size_t)((e && *e) ? atoi(e) : 200) * 1024;
+  size_t want = (size_t)((e && *e) ? atoi(e) : 224) * 1024;
   if (want + fixed > cap) want = cap - fixed;
-  int st = (int)(want / (stage + 16));
-  if (st > 16) st = 16;
-  if (st < 2) st = 2;
-  dl.stages = st;
-  dl.smem = fixed + (size_t)st * (stage + 16);
+  int st = (int)(want / (entry + 16));
+  if (st > 32) st = 32;
+  if (st < 4) st = 4;
+  dl.stages = st;  // ring entries (operand boxes)
+  dl.smem = fixed + (size_t)st * (entry + 16);
   const long long max_items = (long long)p.max_chunks * (p.Hkv / p.decode_hb);
   const char* es = getenv("PATTN_DECODE_SMS");
   const long long g = (long long)std::min(num_sms, std::max(1, (es && *es) ? atoi(es) : num_sms));

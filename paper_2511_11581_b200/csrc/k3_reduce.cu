@@ -8,8 +8,6 @@
 //     M = max_s m_s ;  w_s = 2^{m_s - M} (0 for an empty segment, m_s = -inf)
 //     out[h][:] = sum_s w_s acc_s[:] / sum_s w_s l_s
 // Segments are combined in a fixed order (deterministic; no atomics).
-// Grid: (num_seqs, Hkv * HG, D / 32); each CTA handles 32 head-dim lanes of the <= 8 query
-// heads of one (sequence, KV head, head group); non-decode or unsplit sequences exit at once.
 #include <algorithm>
 
 #include "common.cuh"
@@ -18,113 +16,130 @@
 namespace pattn {
 namespace {
 
-// 64 x kMaxGroups threads = segment groups x 8 heads x 8 float4 columns: thread (sg, h, d4)
-// reduces the segments s = sg (mod SG) of head h for columns 4*d4 .. 4*d4+3 of the item's
-// 32-column slice, then the groups are combined through shared memory in group order
-// (deterministic).  The number of active groups SG = clamp(ceil(n / 8), 1, kMaxGroups) follows
-// the sequence's actual segment count n (config 2: 5 segments -> 1 group; config 4: 37 -> 4);
-// for a given n and launch variant the order of the additions is fixed (bitwise reproducible).
-// Persistent grid (static launch grid): CTAs stride over the (sequence, KV head x
-// head group, 32-column slice) items; sequences that are not split decodes cost one check, so
-// a CUDA-graph bucket padded with empty sequences pays almost nothing for them.
-template <typename T, int D, int kMaxGroups>
-__global__ void __launch_bounds__(64 * kMaxGroups) k3_reduce(Params p) {
-  __shared__ float s_max[kMaxGroups][8];
-  __shared__ float4 s_num[kMaxGroups][8][8];
-  __shared__ float s_den[kMaxGroups][8];
+// One (sequence, query head) item per W warps of a 256-thread CTA (8 / W items per CTA; W = 1
+// for the usual few-segment case, W = 8 for long contexts or forced splitting).  Pass 1: the
+// lanes read the segments' m_s 32 at a time, M = warp max (and, W > 1, CTA max).  Pass 2:
+// segment c goes to warp c mod W of the item, whose lanes cover the D columns (D/32 each,
+// coalesced 512 B per segment row at D = 128); the loop is unrolled so several segments'
+// loads are in flight per warp (the round-1 version walked the segments one dependent load at a
+// time per thread).  W > 1: the warps' (num, den) are combined through shared memory in warp
+// order.  Fixed summation order for a given segment count and W: bitwise reproducible.
+// Persistent grid (static launch grid): CTAs stride over the items; sequences that
+// are not split decodes cost one check, so a padded CUDA-graph bucket pays almost nothing.
+template <typename T, int D, int W>
+__global__ void __launch_bounds__(256) k3_reduce(Params p) {
+  constexpr int kCols = D / 32;   // columns per lane
+  constexpr int kPerCta = 8 / W;  // items per CTA
+  __shared__ float s_num[W > 1 ? 8 : 1][W > 1 ? D : 1];
+  __shared__ float s_red[8][2];
   pdl_wait();  // the decode kernel's partials are complete and visible
-  const int ny = p.Hkv * p.HG, nz = D / 32;
-  const int n_items = p.B * ny * nz;
-  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-    const int b = item / (ny * nz);
-    const int yz = item - b * ny * nz;
-    const int by = yz / nz, bz = yz - by * nz;
-    const int qb = p.cu_seqlens_q[b + 1] - p.cu_seqlens_q[b];
-    if (!(p.decode_split && qb == 1)) continue;
-    const int c0 = p.cu_ch[b];
-    const int n = p.cu_ch[b + 1] - c0;
-    if (n <= 1) continue;  // the decode kernel wrote the final output itself
-    const int groups = min(kMaxGroups, (n + 7) / 8);
-    const int kvh = by / p.HG, hg = by % p.HG;
-    const int g_eff = min(8, p.G - hg * 8);
-    const int head0 = kvh * p.G + hg * 8;
-    const int tok = p.cu_seqlens_q[b];
-    const int d4 = threadIdx.x & 7, h = (threadIdx.x >> 3) & 7, sg = threadIdx.x >> 6;
-    const bool active = h < g_eff && sg < groups;
-    const int d4g = bz * 8 + d4;  // float4 column within the head
-    // 1. M = max_s m_s per head (each group over its segments, then across groups)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int sub = warp / W, wi = warp % W;  // item slot in the CTA, warp within the item
+  const int n_items = p.B * p.Hq;
+  for (int base = blockIdx.x * kPerCta; base < n_items; base += gridDim.x * kPerCta) {
+    const int item = base + sub;
+    int n = 0, c0 = 0, b = 0, h = 0;
+    if (item < n_items) {
+      b = item / p.Hq;
+      h = item - b * p.Hq;
+      const int qb = p.cu_seqlens_q[b + 1] - p.cu_seqlens_q[b];
+      if (p.decode_split && qb == 1) {
+        c0 = p.cu_ch[b];
+        n = p.cu_ch[b + 1] - c0;
+      }
+    }
+    const bool work = n > 1;  // n <= 1: the decode kernel wrote the final output itself
+    // 1. M = max_s m_s
     float M = -INFINITY;
-    if (active)
-      for (int c = sg; c < n; c += groups) M = fmaxf(M, p.part_m[(int64_t)(c0 + c) * p.Hq + head0 + h]);
-    if (d4 == 0) s_max[sg][h] = M;
-    __syncthreads();
-    for (int g = 0; g < groups; ++g) M = fmaxf(M, s_max[g][h]);
+    if (work)
+      for (int c = wi * 32 + lane; c < n; c += 32 * W) M = fmaxf(M, p.part_m[(int64_t)(c0 + c) * p.Hq + h]);
+    M = warp_max(M);
+    if (W > 1) {
+      if (lane == 0) s_red[warp][0] = M;
+      __syncthreads();
+#pragma unroll
+      for (int i = 0; i < W; ++i) M = fmaxf(M, s_red[sub * W + i][0]);
+    }
     // 2. w_s = 2^{m_s - M} (0 for an empty segment); num = sum w_s acc_s, den = sum w_s l_s
-    float den = 0.f;
-    float4 num = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (active) {
-  #pragma unroll 8
-      for (int c = sg; c < n; c += groups) {
-        const int64_t row = (int64_t)(c0 + c) * p.Hq + head0 + h;
+    float num[kCols], den = 0.f;
+#pragma unroll
+    for (int k = 0; k < kCols; ++k) num[k] = 0.f;
+    if (work) {
+#pragma unroll 4
+      for (int c = wi; c < n; c += W) {
+        const int64_t row = (int64_t)(c0 + c) * p.Hq + h;
         const float mc = p.part_m[row];
         const float w = (mc == -INFINITY) ? 0.f : exp2f(mc - M);
         den = fmaf(w, p.part_l[row], den);
-        const float4 a = reinterpret_cast<const float4*>(p.part_acc + row * D)[d4g];
-        num.x = fmaf(w, a.x, num.x);
-        num.y = fmaf(w, a.y, num.y);
-        num.z = fmaf(w, a.z, num.z);
-        num.w = fmaf(w, a.w, num.w);
+        const float* a = p.part_acc + row * D + lane * kCols;
+        if constexpr (kCols == 4) {
+          const float4 v = *reinterpret_cast<const float4*>(a);
+          num[0] = fmaf(w, v.x, num[0]);
+          num[1] = fmaf(w, v.y, num[1]);
+          num[2] = fmaf(w, v.z, num[2]);
+          num[3] = fmaf(w, v.w, num[3]);
+        } else {
+          const float2 v = *reinterpret_cast<const float2*>(a);
+          num[0] = fmaf(w, v.x, num[0]);
+          num[1] = fmaf(w, v.y, num[1]);
+        }
       }
     }
-    s_num[sg][h][d4] = num;
-    if (d4 == 0) s_den[sg][h] = den;
-    __syncthreads();
-    if (sg == 0 && active) {
-      float4 t = s_num[0][h][d4];
-      float dd = s_den[0][h];
-      for (int g = 1; g < groups; ++g) {
-        const float4 u = s_num[g][h][d4];
-        t.x += u.x;
-        t.y += u.y;
-        t.z += u.z;
-        t.w += u.w;
-        dd += s_den[g][h];
+    if (W > 1) {
+#pragma unroll
+      for (int k = 0; k < kCols; ++k) s_num[warp][lane * kCols + k] = num[k];
+      if (lane == 0) s_red[warp][1] = den;
+      __syncthreads();
+      if (wi == 0) {
+        for (int i = 1; i < W; ++i) {
+#pragma unroll
+          for (int k = 0; k < kCols; ++k) num[k] += s_num[warp + i][lane * kCols + k];
+          den += s_red[warp + i][1];
+        }
       }
-      const float inv = 1.f / dd;
-      T* O = static_cast<T*>(p.out) + (int64_t)tok * p.o_st_tok + (int64_t)(head0 + h) * p.o_st_head + d4g * 4;
+    }
+    if (work && wi == 0) {
+      const float inv = 1.f / den;
+      T* O = static_cast<T*>(p.out) + (int64_t)p.cu_seqlens_q[b] * p.o_st_tok + (int64_t)h * p.o_st_head +
+             lane * kCols;
       if constexpr (sizeof(T) == 2) {
-        uint2 packed;
-        packed.x = pack2<T>(t.x * inv, t.y * inv);
-        packed.y = pack2<T>(t.z * inv, t.w * inv);
-        *reinterpret_cast<uint2*>(O) = packed;
+        if constexpr (kCols == 4) {
+          uint2 packed;
+          packed.x = pack2<T>(num[0] * inv, num[1] * inv);
+          packed.y = pack2<T>(num[2] * inv, num[3] * inv);
+          *reinterpret_cast<uint2*>(O) = packed;
+        } else {
+          *reinterpret_cast<uint32_t*>(O) = pack2<T>(num[0] * inv, num[1] * inv);
+        }
       } else {
-        *reinterpret_cast<float4*>(O) = make_float4(t.x * inv, t.y * inv, t.z * inv, t.w * inv);
+        if constexpr (kCols == 4)
+          *reinterpret_cast<float4*>(O) = make_float4(num[0] * inv, num[1] * inv, num[2] * inv, num[3] * inv);
+        else
+          *reinterpret_cast<float2*>(O) = make_float2(num[0] * inv, num[1] * inv);
       }
     }
-    __syncthreads();  // shared partials are reused by the CTA's next item
+    if (W > 1) __syncthreads();  // shared partials are reused by the CTA's next items
   }
 }
 
 }  // namespace
 
-template <typename T, int G>
-cudaError_t launch_reduce_g(const Params& p, int grid, cudaStream_t stream) {
-  if (p.D == 64)
-    return launch_pdl(k3_reduce<T, 64, G>, dim3(grid), dim3(64 * G), 0, stream, p);
-  if (p.D == 128)
-    return launch_pdl(k3_reduce<T, 128, G>, dim3(grid), dim3(64 * G), 0, stream, p);
+template <typename T, int W>
+cudaError_t launch_reduce_w(const Params& p, int grid, cudaStream_t stream) {
+  if (p.D == 64) return launch_pdl(k3_reduce<T, 64, W>, dim3(grid), dim3(256), 0, stream, p);
+  if (p.D == 128) return launch_pdl(k3_reduce<T, 128, W>, dim3(grid), dim3(256), 0, stream, p);
   return cudaErrorInvalidValue;
 }
 
-// Up to 4 segment groups (256 threads) when sequences may have many segments: long contexts
-// (max_seq_len hint > 16384) or forced splitting; the group count actually used follows each
-// sequence's segment count.  Otherwise one group (64 threads, the common few-segment case).
+// Eight warps per item when sequences may have many segments (long contexts: max_seq_len hint
+// > 16384, or forced splitting), else one warp per item.
 template <typename T>
 cudaError_t launch_reduce_t(const Params& p, cudaStream_t stream) {
-  const long long items = (long long)p.B * p.Hkv * p.HG * (p.D / 32);
   const bool many = p.max_seq_len_hint > 16384 || p.split_mode == 2;
-  const int grid = (int)std::min<long long>(items, (long long)p.num_sms * (many ? 8 : 16));
-  return many ? launch_reduce_g<T, 4>(p, std::max(grid, 1), stream) : launch_reduce_g<T, 1>(p, std::max(grid, 1), stream);
+  const int per_cta = many ? 1 : 8;
+  const long long ctas = ((long long)p.B * p.Hq + per_cta - 1) / per_cta;
+  const int grid = (int)std::max<long long>(1, std::min<long long>(ctas, (long long)p.num_sms * 8));
+  return many ? launch_reduce_w<T, 8>(p, grid, stream) : launch_reduce_w<T, 1>(p, grid, stream);
 }
 
 cudaError_t launch_reduce(const Params& p, cudaStream_t stream) {

@@ -376,9 +376,9 @@ def test_strided_out_and_q_canary():
 
 @pytest.mark.parametrize("flags", [0, 0x4])
 def test_segment_reduce_groups_follow_segment_count(flags):
-    """K3 picks its segment-group count from each sequence's actual number of segments (1 group
-    for a few, up to 4 for many): sequences from 1 to several hundred segments in one batch,
-    against the oracle, and bitwise reproducible."""
+    """K3 on sequences from 1 to several hundred segments in one batch (one warp per (sequence,
+    head) item, or eight for long contexts / forced splitting), against the oracle, and bitwise
+    reproducible."""
     w = Workload("k3groups", ((20000, 1), (0, 40), (3000, 1), (17, 1), (9000, 1), (60000, 1)), 64, 8, 128, 16,
                  "bf16")
     batch = generate(w, seed=13, dist="peaked")
