@@ -42,8 +42,10 @@
  *     PATTN_ERR_INVALID_SEQUENCE in that case (debugging aid; not for the hot path, and
  *     skipped while the stream is being captured into a CUDA graph).
  *   - Environment overrides of the planner (sweeps and A/B only): PATTN_ITEMS_PER_SM,
- *     PATTN_MIN_CHUNK_TOKENS, PATTN_DECODE_CTAS, PATTN_K2_SM_GBS, PATTN_SERIAL (see
- *     pattn_tuning_t), PATTN_PREFILL_SMS (fixed two-stream split), PATTN_DISABLE_K1.
+ *     PATTN_MIN_CHUNK_TOKENS, PATTN_DECODE_CTAS, PATTN_K2_SM_GBS, PATTN_SERIAL,
+ *     PATTN_DECODE_WIDE (1 / 0 = decode_kernel 1 / 2) (see pattn_tuning_t),
+ *     PATTN_PREFILL_SMS (fixed two-stream split), PATTN_DISABLE_K1, PATTN_DECODE_WIDE_HB
+ *     (cap on K2W's heads per box).
  */
 #ifndef PATTN_H_
 #define PATTN_H_
@@ -227,14 +229,17 @@ PATTN_API pattn_status_t pattn_write_kv(const pattn_problem_t* p, const void* k_
  * Precedence: PATTN_* environment overrides > the loaded tree > built-in defaults.
  */
 typedef struct pattn_tuning {
-  int32_t items_per_sm;       /* decode: target (segment x KV head x head group) work items per SM (default 16) */
-  int32_t min_chunk_tokens;   /* decode: shortest split segment, in keys (default 256) */
-  int32_t decode_ctas_per_sm; /* decode: resident K2 CTAs per SM, 1..4 (default 2) */
+  int32_t items_per_sm;       /* decode: target work items per SM -- K2: (segment x KV head x head group),
+                                 K2W: (segment x group of HB KV heads) -- (default 16 for K2, 2 for K2W) */
+  int32_t min_chunk_tokens;   /* decode: shortest split segment, in keys (default 256 for K2, 128 for K2W) */
+  int32_t decode_ctas_per_sm; /* decode: resident K2 CTAs per SM, 1..4 (default 2; K2W runs one) */
   int32_t k2_sm_mbs;          /* mixed batches, two streams: decode streaming rate per SM (MB/s) that K5's
                                  SM-partition model assumes -- higher leaves more SMs to the prefill kernel
                                  (default: the measured rate of the decode kernel in use, K2W 80000, K2 61000) */
   int32_t serial;             /* mixed batches: 1 = prefill and decode kernels back to back on one stream
                                  even when a second stream is given; 0 = concurrent (default) */
+  int32_t decode_kernel;      /* decode kernel: 1 = K2W (head-wide TMA boxes) where it applies (G <= 8,
+                                 2 | Hkv), 2 = K2 (one KV head per work item); default 1 */
 } pattn_tuning_t;           /* 0 in a field = built-in default */
 
 enum {

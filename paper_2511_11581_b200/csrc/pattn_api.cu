@@ -124,7 +124,7 @@ TuningTree& tuning_tree() {
 bool leaf_ok(const pattn_tuning_t& t) {
   return t.items_per_sm >= 0 && t.items_per_sm <= 4096 && t.min_chunk_tokens >= 0 && t.min_chunk_tokens <= (1 << 24) &&
          t.decode_ctas_per_sm >= 0 && t.decode_ctas_per_sm <= 4 && t.k2_sm_mbs >= 0 && t.k2_sm_mbs <= 1000000 &&
-         (t.serial == 0 || t.serial == 1);
+         (t.serial == 0 || t.serial == 1) && t.decode_kernel >= 0 && t.decode_kernel <= 2;
 }
 
 double feature_value(const pattn_problem_t* p, int f) {
@@ -140,7 +140,7 @@ double feature_value(const pattn_problem_t* p, int f) {
 
 // Tree leaf for p (all zero when no tree is loaded), then env overrides, then defaults.
 pattn_tuning_t resolve_tuning(const pattn_problem_t* p) {
-  pattn_tuning_t t{0, 0, 0, 0, 0};
+  pattn_tuning_t t{0, 0, 0, 0, 0, 0};
   {
     TuningTree& tt = tuning_tree();
     std::lock_guard<std::mutex> g(tt.mu);
@@ -159,8 +159,10 @@ pattn_tuning_t resolve_tuning(const pattn_problem_t* p) {
   if ((e = getenv("PATTN_DECODE_CTAS")) && *e) t.decode_ctas_per_sm = atoi(e);
   if ((e = getenv("PATTN_K2_SM_GBS")) && *e) t.k2_sm_mbs = (int32_t)(atof(e) * 1000.0);
   if ((e = getenv("PATTN_SERIAL")) && *e) t.serial = atoi(e) ? 1 : 0;
-  if (t.items_per_sm <= 0) t.items_per_sm = 16;
-  if (t.min_chunk_tokens <= 0) t.min_chunk_tokens = 256;
+  if ((e = getenv("PATTN_DECODE_WIDE")) && *e) t.decode_kernel = atoi(e) ? 1 : 2;
+  if (t.decode_kernel <= 0) t.decode_kernel = 1;
+  // items_per_sm and min_chunk_tokens stay 0 here: their defaults depend on the decode kernel
+  // (make_plan: K2 16 items per SM and 256-key segments, K2W 2 and 128)
   if (t.decode_ctas_per_sm <= 0) t.decode_ctas_per_sm = 2;
   if (t.decode_ctas_per_sm > 4) t.decode_ctas_per_sm = 4;
   return t;
@@ -290,7 +292,18 @@ pattn_status_t make_plan(const pattn_problem_t* p, const void* q, const void* kc
   const int bm = pl->block_q * G;
   pl->rpw = bm <= 32 ? 8 : 16;
 
-  // decode segment policy (parallel tiled softmax): ~8 items per SM by default
+  // Decode kernel.  K2W: decode items of HB KV heads (one TMA request per 16 keys x HB heads;
+  // default whenever G <= 8 and 2 | Hkv, tuning decode_kernel 2 / PATTN_DECODE_WIDE=0 keeps K2).
+  if (pl->use_k2 && pl->tuning.decode_kernel != 2) pl->decode_hb = wide_decode_heads(p->num_kv_heads, G);
+  // Decode segment policy (parallel tiled softmax): target work items per SM and the
+  // shortest segment.  The tuning leaf's values apply to the kernel it was measured with (its
+  // decode_kernel); otherwise the kernel's defaults: K2 16 items per SM and 256-key segments; K2W,
+  // whose items are HB x larger, 2 and 128 (the tuning sweep's best single configuration,
+  // profiles/r02/tuning_holdout.json; more segments cost K3 partial traffic: config 4 at 32 per SM
+  // wrote 153 MB of partials).
+  const bool leaf_fits = (pl->decode_hb > 0) == (pl->tuning.decode_kernel != 2);
+  const int items_per_sm = leaf_fits && pl->tuning.items_per_sm > 0 ? pl->tuning.items_per_sm : (pl->decode_hb ? 2 : 16);
+  const int min_tok = leaf_fits && pl->tuning.min_chunk_tokens > 0 ? pl->tuning.min_chunk_tokens : (pl->decode_hb ? 128 : 256);
   if (p->flags & PATTN_FLAG_NO_SPLIT) {
     pl->split_mode = 1;
     pl->target_items = 1;
@@ -300,20 +313,11 @@ pattn_status_t make_plan(const pattn_problem_t* p, const void* q, const void* kc
     pl->target_items = pl->num_sms * 64;
     pl->min_chunk = 1;
   } else {
-    pl->target_items = env_int("PATTN_TARGET_ITEMS", pl->num_sms * pl->tuning.items_per_sm);
-    pl->min_chunk = env_int("PATTN_MIN_CHUNK_BLOCKS",
-                            std::max(1, (pl->tuning.min_chunk_tokens + p->block_size - 1) / p->block_size));
+    pl->target_items = env_int("PATTN_TARGET_ITEMS", pl->num_sms * items_per_sm);
+    pl->min_chunk = env_int("PATTN_MIN_CHUNK_BLOCKS", std::max(1, (min_tok + p->block_size - 1) / p->block_size));
   }
   if (pl->target_items < 1) pl->target_items = 1;
   if (pl->min_chunk < 1) pl->min_chunk = 1;
-  // K2W: decode items of HB KV heads (one TMA request per 16 keys x HB heads; default whenever
-  // G <= 8 and 2 | Hkv, PATTN_DECODE_WIDE=0 keeps K2).  Its items are HB x larger than K2's, so
-  // the segment plan targets fewer of them: 4 per SM (measured best of 4 / 8 / 16 on configs 2-5;
-  // more segments cost K3 partial traffic: config 4 at 32 per SM wrote 153 MB of partials).
-  if (pl->use_k2 && env_int("PATTN_DECODE_WIDE", 1)) pl->decode_hb = wide_decode_heads(p->num_kv_heads, G);
-  if (pl->decode_hb && !(p->flags & (PATTN_FLAG_NO_SPLIT | PATTN_FLAG_FORCE_SPLIT))) {
-    pl->target_items = std::max(1, env_int("PATTN_TARGET_ITEMS", pl->num_sms * env_int("PATTN_WIDE_ITEMS_PER_SM", 4)));
-  }
   const long long units = (long long)p->num_kv_heads * pl->HG;
   const long long seg_units = pl->k4_decodes  ? (long long)p->num_kv_heads  // K4: all G heads per item
                               : pl->decode_hb ? (long long)(p->num_kv_heads / pl->decode_hb)

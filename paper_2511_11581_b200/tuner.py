@@ -14,6 +14,7 @@ Here a configuration is the planner's launch knobs (pattn_tuning_t, include/patt
   k2_sm_mbs           mixed batches: the per-SM decode rate K5's SM-partition model assumes
                       (shifts SMs between the concurrent prefill and decode kernels)
   serial              mixed batches: prefill and decode back to back instead of concurrent
+  decode_kernel       1 = K2W (head-wide TMA boxes, where it applies), 2 = K2 (one KV head per item)
 (0 = the built-in default for any knob).
 and the features are the host-known batch quantities the planner sees (PATTN_FEAT_*):
 num_seqs, num_tokens, max_query_len (1 = decode-only batch), max_seq_len.
@@ -31,12 +32,15 @@ import math
 from typing import Dict, Iterable, List, Optional, Sequence, Tuple
 
 FEATURES = ["num_seqs", "num_tokens", "max_query_len", "max_seq_len"]  # order = PATTN_FEAT_*
-KNOBS = ["items_per_sm", "min_chunk_tokens", "decode_ctas_per_sm", "k2_sm_mbs", "serial"]
+KNOBS = ["items_per_sm", "min_chunk_tokens", "decode_ctas_per_sm", "k2_sm_mbs", "serial", "decode_kernel"]
 
 
 # libpattn's built-in value of each knob (used where a tree leaf or record holds 0)
-# k2_sm_mbs 0: the measured per-SM rate of the decode kernel the planner picks (K2W 80 GB/s, K2 61 GB/s)
-DEFAULTS = {"items_per_sm": 16, "min_chunk_tokens": 256, "decode_ctas_per_sm": 2, "k2_sm_mbs": 0, "serial": 0}
+# 0 where the default depends on the decode kernel the planner picks: items_per_sm (K2 16, K2W 2),
+# min_chunk_tokens (K2 256, K2W 128),
+# k2_sm_mbs (the kernel's measured per-SM rate: K2W 80 GB/s, K2 61 GB/s)
+DEFAULTS = {"items_per_sm": 0, "min_chunk_tokens": 0, "decode_ctas_per_sm": 2, "k2_sm_mbs": 0, "serial": 0,
+            "decode_kernel": 1}
 
 
 def with_defaults(cfg: Dict) -> Dict:
@@ -80,8 +84,12 @@ def _best_config(labels, table):
     return best, _regret(labels, table, best)
 
 
-def fit_decision_tree(records: Sequence[Dict], max_depth: int = 3) -> Dict:
-    """Greedy regret-minimising tree (JSON form).  Raises NoData on empty input."""
+def fit_decision_tree(records: Sequence[Dict], max_depth: int = 3, min_gain: float = 0.0) -> Dict:
+    """Greedy regret-minimising tree (JSON form).  Raises NoData on empty input.
+
+    min_gain: a split must lower the node's summed regret by at least this fraction of the
+    summed best latency of the node's scenarios (a noise floor: run-to-run spread is ~1 %, and a
+    split that only chases it does not carry over to unseen scenarios)."""
     table = _scenario_table(records)
     if not table:
         raise NoData("no tuning records")
@@ -91,6 +99,7 @@ def fit_decision_tree(records: Sequence[Dict], max_depth: int = 3) -> Dict:
         leaf = {k: v for k, v in zip(KNOBS, key)}
         if depth >= max_depth or reg <= 0.0 or len(labels) < 2:
             return leaf
+        floor = min_gain * sum(min(table[lab][1].values()) for lab in labels)
         best = None
         for fi, f in enumerate(FEATURES):
             vals = sorted({table[lab][0][f] for lab in labels})
@@ -102,7 +111,7 @@ def fit_decision_tree(records: Sequence[Dict], max_depth: int = 3) -> Dict:
                 cand = (r, fi, thr)
                 if best is None or cand < best:
                     best = (r, fi, thr, lt, ge)
-        if best is None or best[0] >= reg:
+        if best is None or best[0] >= reg or reg - best[0] < floor:
             return leaf
         _, fi, thr, lt, ge = best
         return {"feature": FEATURES[fi], "threshold": thr, "lt": build(lt, depth + 1), "ge": build(ge, depth + 1)}

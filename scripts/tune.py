@@ -14,8 +14,9 @@ of the tuning".
 Per scenario the unified call is timed with CUDA events (the paper's protocol: 20
 warm-up, mean of 100), after checking that the configuration's output equals the default
 configuration's within the bf16 tolerance (tuning never changes the math):
-  stage 1  the decode knobs (items_per_sm x min_chunk_tokens x decode_ctas_per_sm, 64 configs)
-           with the partition knobs at their defaults;
+  stage 1  the decode kernel and its knobs (K2W: items_per_sm x min_chunk_tokens, 16 configs;
+           K2: items_per_sm x min_chunk_tokens x decode_ctas_per_sm, 64) with the partition
+           knobs at their defaults;
   stage 2  mixed batches only: the partition knobs (k2_sm_mbs -- the decode rate per SM that
            K5's SM-partition model assumes -- and serial) at the stage-1 best decode knobs.
            For decode-only batches the partition knobs have no effect; their stage-1 records
@@ -74,9 +75,13 @@ def holdout_scenarios():
     ]
 
 
-DECODE_GRID = [dict(zip(tuner.KNOBS[:3], v)) for v in itertools.product([4, 8, 16, 32], [128, 256, 1024, 4096],
-                                                                         [1, 2, 3, 4])]
-PARTITION_GRID = [{"k2_sm_mbs": v, "serial": 0} for v in (45000, 61000, 80000, 100000)] + [{"k2_sm_mbs": 0, "serial": 1}]
+# decode kernel x its knobs: K2W (decode_kernel 1, one CTA per SM) and K2 (2, 1-4 CTAs per SM)
+DECODE_GRID = ([{"items_per_sm": i, "min_chunk_tokens": m, "decode_ctas_per_sm": 1, "decode_kernel": 1}
+                for i, m in itertools.product([2, 4, 8, 16], [128, 256, 1024, 4096])] +
+               [{"items_per_sm": i, "min_chunk_tokens": m, "decode_ctas_per_sm": c, "decode_kernel": 2}
+                for i, m, c in itertools.product([4, 8, 16, 32], [128, 256, 1024, 4096], [1, 2, 3, 4])])
+PARTITION_GRID = ([{"k2_sm_mbs": v, "serial": 0} for v in (45000, 61000, 80000, 100000, 120000)] +
+                  [{"k2_sm_mbs": 0, "serial": 1}])
 
 
 def full(cfg):
@@ -154,6 +159,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--iters", type=int, default=100)
     ap.add_argument("--depth", type=int, default=4)
+    ap.add_argument("--min-gain", type=float, default=0.005,
+                    help="a split must cut the node's regret by this fraction of its summed best latency")
     args = ap.parse_args()
     os.makedirs(args.out, exist_ok=True)
     paths = {k: os.path.join(args.out, f"tuning_records{k}.ndjson") for k in ("", "_holdout")}
@@ -172,9 +179,13 @@ def main():
         del b
         torch.cuda.empty_cache()
     train = tuner.read_records(paths[""])
-    tree = tuner.fit_decision_tree(train, max_depth=args.depth)
+    tree = tuner.fit_decision_tree(train, max_depth=args.depth, min_gain=args.min_gain)
+    unreg = tuner.fit_decision_tree(train, max_depth=args.depth)  # for the report: the unregularised fit
     print(tuner.to_pseudocode(tree))
     report = {"train": {"scenarios": len({r["scenario"] for r in train}),
+                        "tree_depth": tuner.depth(tree), "min_gain": args.min_gain,
+                        "unregularised_tree_depth": tuner.depth(unreg),
+                        "unregularised_tree_regret_us": tuner.tree_regret(unreg, train),
                         "tree_regret_us": tuner.tree_regret(tree, train),
                         "best_single_config_regret_us": tuner.best_global_regret(train)},
               "holdout": []}
@@ -184,7 +195,8 @@ def main():
         b, recs = sweep(w, dev, s1, s2, args)
         choice = full(tuner.select(tree, features(w)))
         single = full(best_single)
-        for c in (choice, single):
+        unreg_choice = full(tuner.select(unreg, features(w)))
+        for c in (choice, single, unreg_choice, full({})):
             if all(r["config"] != c for r in recs):  # (replicated decode-only records count: exact)
                 recs.append(b.record(c))
         tuner.write_records(paths["_holdout"], recs)
@@ -193,6 +205,7 @@ def main():
         dflt = table.get(tuner.config_key(full({})), float("nan"))
         entry = {"scenario": w.name, "features": features(w), "best_us": best,
                  "tree_choice": choice, "tree_us": table[tuner.config_key(choice)],
+                 "unregularised_tree_us": table[tuner.config_key(unreg_choice)],
                  "best_single_train_config_us": table[tuner.config_key(single)], "default_us": dflt}
         entry["tree_regret_us"] = entry["tree_us"] - best
         report["holdout"].append(entry)
@@ -203,6 +216,7 @@ def main():
     ho = report["holdout"]
     report["holdout_summary"] = {
         "scenarios": len(ho), "tree_regret_us": sum(e["tree_regret_us"] for e in ho),
+        "unregularised_tree_regret_us": sum(e["unregularised_tree_us"] - e["best_us"] for e in ho),
         "best_single_train_config_regret_us": sum(e["best_single_train_config_us"] - e["best_us"] for e in ho),
         "default_regret_us": sum(e["default_us"] - e["best_us"] for e in ho),
         "sum_best_us": sum(e["best_us"] for e in ho)}

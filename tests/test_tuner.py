@@ -8,9 +8,12 @@ import pytest
 
 from paper_2511_11581_b200 import tuner
 
-A = {"items_per_sm": 16, "min_chunk_tokens": 256, "decode_ctas_per_sm": 2, "k2_sm_mbs": 0, "serial": 0}
-B = {"items_per_sm": 4, "min_chunk_tokens": 1024, "decode_ctas_per_sm": 3, "k2_sm_mbs": 80000, "serial": 0}
-C = {"items_per_sm": 32, "min_chunk_tokens": 64, "decode_ctas_per_sm": 1, "k2_sm_mbs": 45000, "serial": 1}
+A = {"items_per_sm": 0, "min_chunk_tokens": 0, "decode_ctas_per_sm": 2, "k2_sm_mbs": 0, "serial": 0,
+     "decode_kernel": 1}  # = libpattn's built-in defaults
+B = {"items_per_sm": 4, "min_chunk_tokens": 1024, "decode_ctas_per_sm": 3, "k2_sm_mbs": 80000, "serial": 0,
+     "decode_kernel": 2}
+C = {"items_per_sm": 32, "min_chunk_tokens": 64, "decode_ctas_per_sm": 1, "k2_sm_mbs": 45000, "serial": 1,
+     "decode_kernel": 1}
 
 
 def _rec(label, feats, cfg, mean):
@@ -41,6 +44,21 @@ def test_decode_only_vs_prefill_split_on_max_query_len():
     assert tuner.select(tree, _feats(3, 3, 1, 100)) == B
     assert tuner.select(tree, _feats(3, 9000, 2048, 100)) == A
     assert tuner.tree_regret(tree, recs) == 0.0
+
+
+def test_min_gain_suppresses_noise_splits():
+    # two scenario classes whose best configs differ by 0.3 % (noise-level) vs 30 %: with a 1 %
+    # noise floor only the large difference may split the tree
+    def recs(gap):
+        out = []
+        for i, (maxq, best, ns) in enumerate([(1, B, 16), (1, B, 64), (2048, A, 32), (512, A, 8)]):
+            f = _feats(ns, ns if maxq == 1 else 4096, maxq, 8192)
+            other = A if best is B else B
+            out += [_rec(f"s{i}", f, best, 100.0), _rec(f"s{i}", f, other, 100.0 + gap)]
+        return out
+    assert tuner.depth(tuner.fit_decision_tree(recs(0.3), max_depth=3)) == 1  # unregularised: splits
+    assert tuner.depth(tuner.fit_decision_tree(recs(0.3), max_depth=3, min_gain=0.01)) == 0
+    assert tuner.depth(tuner.fit_decision_tree(recs(30.0), max_depth=3, min_gain=0.01)) == 1
 
 
 def test_tree_regret_never_worse_than_best_global_config():
