@@ -16,7 +16,7 @@ def load(path):
     agg = defaultdict(lambda: defaultdict(list))
     for i, m in per.items():
         n = names[i]
-        short = next((k for k in ("k1_prefill", "k2_decode", "k3_reduce", "k4_generic", "k5_metadata") if k in n), n[:40])
+        short = next((k for k in ("k1_prefill", "k2w_decode", "k2_decode", "k3_reduce", "k4_generic", "k5_metadata") if k in n), n[:40])
         for k, v in m.items():
             agg[short][k].append(v)
     return agg

@@ -68,10 +68,11 @@ def main(rnd):
                 n = len(t)
                 lines.append(f"  {k:12s} launches {n:3d} mean {sum(t)/n/1e3:9.2f} us share {sum(t)/tot:6.1%} "
                              f"dram rd {sum(rd)/n/1e6:9.2f} MB wr {sum(wr)/n/1e6:8.2f} MB")
-                name = {"k1_prefill": "prefill", "k2_decode": "decode", "k3_reduce": "reduce",
+                name = {"k1_prefill": "prefill", "k2_decode": "decode", "k2w_decode": "decode", "k3_reduce": "reduce",
                         "k4_generic": "generic", "k5_metadata": "metadata"}.get(k, k)
                 traffic.setdefault(wl, {})[name] = (sum(rd) + sum(wr)) / n
-    for rep in ("k1_c3_full", "k1_c3p_full", "k2_c2_full", "k2_c4_full", "k2_sm36", "k3_c4_full", "k6_c3_full"):
+    for rep in ("k1_c3_full", "k1_c3p_full", "k2_c2_full", "k2_c4_full", "k2_sm36", "k2w_c2_full", "k2w_c4_full",
+                "k2w_sm36_main", "k3_c4_full", "k6_c3_full"):
         path = os.path.join(src, rep + ".ncu-rep")
         if os.path.exists(path):
             shutil.copy(path, os.path.join(dst, rep + ".ncu-rep"))
