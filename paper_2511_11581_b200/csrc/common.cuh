@@ -266,6 +266,16 @@ PATTN_DEVICE void tma_store_4d(const CUtensorMap* m, const void* smem_src, int c
       "r"(smem_u32(smem_src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
       : "memory");
 }
+// 16-byte global -> shared copy (LDGSTS, L2 only) with an L2 cache-policy hint.
+PATTN_DEVICE void cp_async_16_hint(uint32_t dst, const void* src, uint64_t policy) {
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "l"(policy)
+               : "memory");
+}
+// Arrive on `bar` once all of this thread's prior cp.async have completed; the arrival counts
+// against the barrier's initial count (noinc).
+PATTN_DEVICE void cp_async_mbar_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
 PATTN_DEVICE void bulk_commit_group() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
 // Wait until every committed bulk store of this thread has finished READING its shared source.
 PATTN_DEVICE void bulk_wait_group_read0() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }

@@ -48,6 +48,7 @@ struct WideShape {
 
 struct WItem {
   int b, c, hb, sb0, sb1, nseg, L, tok;
+  int k0, k1;  // the segment's keys [k0, k1): sub-block j holds keys k0 + 16 j ..
 };
 
 // Segment c of decode sequence b covers paged blocks [kb0, kb1) of K5's plan (the same
@@ -65,14 +66,20 @@ __device__ __forceinline__ WItem wide_item(const Params& p, int it, int ngroups)
   const int per = (nblk + x.nseg - 1) / x.nseg;
   const int kb0 = (x.c - c0) * per;
   const int kb1 = min(nblk, kb0 + per);
-  const int n16 = p.bs / kSub;
+  x.k0 = kb0 * p.bs;
+  x.k1 = min(kb1 * p.bs, x.L);
+  const int n16 = p.bs / kSub;  // TMA path (bs a multiple of 16): sub-blocks are page-aligned
   x.sb0 = kb0 * n16;
-  x.sb1 = min(kb1 * n16, (x.L + kSub - 1) / kSub);
+  x.sb1 = x.sb0 + (x.k1 - x.k0 + kSub - 1) / kSub;
   return x;
 }
 
-template <int D, int HB, typename E>
-__global__ void __launch_bounds__((HB + 1) * 32, 1)
+// kGather: block sizes that are not a multiple of 16 (no TMA box fits a page): four producer
+// warps gather the same ring entries row by row with 16-byte cp.async (one block-table lookup per
+// key row, any block size, 16-byte aligned rows), completing on the entry's mbarrier through
+// cp.async.mbarrier.arrive.noinc; the consumers are unchanged.
+template <int D, int HB, typename E, bool kGather>
+__global__ void __launch_bounds__((HB + (kGather ? 4 : 1)) * 32, 1)
     k2w_decode(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, Params p,
                int nent) {
   using S = WideShape<D, HB>;
@@ -87,6 +94,7 @@ __global__ void __launch_bounds__((HB + 1) * 32, 1)
   uint64_t* item_empty = item_full + kItemRing;
   volatile int* item_ring = reinterpret_cast<volatile int*>(item_empty + kItemRing);
 
+  constexpr int kProd = kGather ? 4 : 1;  // producer warps
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   pdl_wait();  // K5's metadata (or, serial, the previous kernel's work) is complete and visible
   if (p.partition) {
@@ -103,12 +111,12 @@ __global__ void __launch_bounds__((HB + 1) * 32, 1)
   }
   if (threadIdx.x == 0) {
     for (int s = 0; s < nent; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], kGather ? kProd * 32 : 1);  // gather: one noinc arrive per producer thread
       mbar_init(&empty[s], HB);
     }
     for (int i = 0; i < kItemRing; ++i) {
       mbar_init(&item_full[i], 1);
-      mbar_init(&item_empty[i], HB);
+      mbar_init(&item_empty[i], HB + kProd - 1);  // consumers + the other producer warps
     }
     fence_barrier_init();
   }
@@ -118,7 +126,70 @@ __global__ void __launch_bounds__((HB + 1) * 32, 1)
   const int n_items = p.hdr[kHdrTotalChunks] * ngroups;
   const int n16 = p.bs / kSub;
 
-  if (warp == 0) {
+  if (kGather && warp < kProd) {
+    // ------------------------------------------------------------ gather producers
+    // Thread i of the 128 owns key row t = i / 8 of every sub-block and 16-byte chunk ch = i % 8
+    // of each 128-byte row segment: per entry it issues HB x D/64 cp.async into the entry's
+    // swizzled [head][half][slot][64 d] layout (the TMA box layout) and one noinc arrive.
+    const int tid = threadIdx.x, t = tid >> 3, ch = tid & 7;
+    const uint64_t policy = l2_policy_evict_first();
+    const int esz = (int)sizeof(typename E::T);
+    uint32_t s = 0, ph = 0;
+    for (uint32_t ni = 0;; ++ni) {
+      int it = 0;
+      const uint32_t slot = ni % kItemRing;
+      if (warp == 0) {
+        if (lane == 0) {
+          mbar_wait(&item_empty[slot], ((ni / kItemRing) & 1u) ^ 1u);
+          it = atomicAdd(p.hdr + kHdrDecodeCounter, 1);
+          item_ring[slot] = it;
+          mbar_arrive(&item_full[slot]);
+        }
+        it = __shfl_sync(0xffffffffu, it, 0);
+      } else {
+        mbar_wait(&item_full[slot], (ni / kItemRing) & 1u);
+        it = item_ring[slot];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&item_empty[slot]);
+      }
+      if (it >= n_items) {
+        if (warp == 0 && lane == 0) pdl_trigger();
+        break;
+      }
+      const WItem x = wide_item(p, it, ngroups);
+      const int32_t* bt = p.block_table + (int64_t)x.b * p.bt_stride;
+      const int nsb = (x.k1 - x.k0 + kSub - 1) / kSub;
+      for (int j = 0; j < nsb; ++j) {
+        const int key = x.k0 + j * kSub + t;
+        const uint8_t* srck = nullptr;
+        int64_t row = 0;
+        if (key < x.k1) {
+          const int pg = key / p.bs;
+          row = ((int64_t)__ldg(bt + pg) * p.kv_st_blk + (int64_t)(key - pg * p.bs) * p.kv_st_tok +
+                 (int64_t)(x.hb * HB) * p.kv_st_head + ch * 8) * esz;
+          srck = static_cast<const uint8_t*>(p.k);
+        }
+#pragma unroll
+        for (int op = 0; op < 2; ++op) {  // K, then V
+          mbar_wait(&empty[s], ph ^ 1u);
+          if (srck) {
+            const uint8_t* src = static_cast<const uint8_t*>(op ? p.v : p.k) + row;
+            const uint32_t dst = smem_u32(ring + (size_t)s * S::kOpBytes) + t * 128 + ((ch ^ (t & 7)) << 4);
+#pragma unroll
+            for (int h = 0; h < HB; ++h)
+#pragma unroll
+              for (int hf = 0; hf < S::kHalves; ++hf)
+                cp_async_16_hint(dst + h * S::kHeadBytes + hf * S::kHalfBytes,
+                                 src + ((int64_t)h * p.kv_st_head + hf * 64) * esz, policy);
+          }
+          cp_async_mbar_arrive_noinc(&full[s]);
+          if (++s == (uint32_t)nent) s = 0, ph ^= 1u;
+        }
+      }
+    }
+    return;
+  }
+  if (!kGather && warp == 0) {
     // ------------------------------------------------------------ producer
     if (lane == 0) {
       tma_prefetch_desc(&tmK);
@@ -167,7 +238,7 @@ __global__ void __launch_bounds__((HB + 1) * 32, 1)
   }
 
   // -------------------------------------------------------------- consumers (one KV head each)
-  const int w = warp - 1;
+  const int w = warp - kProd;
   const int r = lane >> 2, c = lane & 3;       // mma fragment coordinates
   const int mat = lane >> 3, mrow = lane & 7;  // ldmatrix source coordinates
   using ET = typename E::T;
@@ -202,7 +273,7 @@ __global__ void __launch_bounds__((HB + 1) * 32, 1)
 #pragma unroll
     for (int t = 0; t < S::kKC; ++t) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0.f;
 
-    const int nsb = x.sb1 - x.sb0;
+    const int nsb = (x.k1 - x.k0 + kSub - 1) / kSub;
     for (int j = 0; j < nsb; ++j) {
       mbar_wait(&full[s], ph);  // K(j)
       const uint32_t kst = ring_u32 + s * S::kOpBytes + w * S::kHeadBytes;
@@ -231,7 +302,7 @@ __global__ void __launch_bounds__((HB + 1) * 32, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[ks]);  // K(j) consumed (the ldmatrix results fed the mma)
       mbar_wait(&full[vs], vph);
-      const int valid = x.L - (x.sb0 + j) * kSub;  // slots [0, valid) hold real keys
+      const int valid = x.k1 - (x.k0 + j * kSub);  // rows [0, valid) hold this segment's keys
       if (valid < kSub) {
         // zero this head's V rows past the sequence end (NaN * 0 = NaN inside the mma)
         uint8_t* vgen = ring + (size_t)vs * S::kOpBytes + w * S::kHeadBytes;
@@ -349,13 +420,19 @@ __global__ void __launch_bounds__((HB + 1) * 32, 1)
   }
 }
 
+template <int D, int HB, typename E, bool G>
+cudaError_t launch_wg(const Params& p, const DecodeLaunch& dl, const CUtensorMap& tmK, const CUtensorMap& tmV,
+                      cudaStream_t stream) {
+  auto kern = k2w_decode<D, HB, E, G>;
+  cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(kern), dl.smem);
+  if (e != cudaSuccess) return e;
+  return launch_pdl(kern, dim3(dl.grid), dim3((HB + (G ? 4 : 1)) * 32), dl.smem, stream, tmK, tmV, p, dl.stages);
+}
 template <int D, int HB, typename E>
 cudaError_t launch_w(const Params& p, const DecodeLaunch& dl, const CUtensorMap& tmK, const CUtensorMap& tmV,
                      cudaStream_t stream) {
-  auto kern = k2w_decode<D, HB, E>;
-  cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(kern), dl.smem);
-  if (e != cudaSuccess) return e;
-  return launch_pdl(kern, dim3(dl.grid), dim3((HB + 1) * 32), dl.smem, stream, tmK, tmV, p, dl.stages);
+  return p.decode_gather ? launch_wg<D, HB, E, true>(p, dl, tmK, tmV, stream)
+                         : launch_wg<D, HB, E, false>(p, dl, tmK, tmV, stream);
 }
 
 template <int D, typename E>

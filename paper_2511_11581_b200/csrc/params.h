@@ -43,6 +43,7 @@ struct Params {
   int32_t min_chunk_blocks;
   int32_t num_sms;
   int32_t decode_hb;      // > 0: decode on K2W, HB KV heads per TMA box / work item (Hkv / HB items per segment)
+  int32_t decode_gather;  // K2W: 1 -> entries gathered row by row with cp.async (block size not a multiple of 16)
   int32_t kv_tok_inner;   // TMA dim order: 1 -> (d, slot, kvh, blk) [HND], 0 -> (d, kvh, slot, blk) [NHD]
   // Two-stream SM partition (K1 and K2 concurrent): K5 picks the number of SMs P for the
   // prefill kernel from the batch (cost model below); K1 CTAs >= P exit at once so that the

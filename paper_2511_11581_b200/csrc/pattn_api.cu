@@ -174,6 +174,7 @@ struct Plan {
   bool kv_vec16 = false;    // K/V rows 16-byte aligned (K4 vector loads)
   int block_q = 1, HG = 1, rpw = 8;
   int decode_hb = 0;  // > 0: decodes on K2W (head-wide boxes)
+  bool decode_gather = false;  // K2W with cp.async-gathered entries (block size not a multiple of 16)
   int target_items = 0, min_chunk = 1, split_mode = 0, max_chunks = 0;
   int num_sms = 148;
   size_t max_smem = 0;
@@ -217,6 +218,7 @@ void fill_params(const pattn_problem_t* p, const Plan& pl, Params* k) {
   k->block_q = pl.block_q;
   k->HG = pl.HG;
   k->decode_hb = pl.decode_hb;
+  k->decode_gather = pl.decode_gather ? 1 : 0;
   k->max_chunks = pl.max_chunks;
   k->decode_split = (pl.use_k2 || pl.k4_decodes) ? 1 : 0;
   k->k4_decodes = pl.k4_decodes ? 1 : 0;
@@ -261,9 +263,21 @@ pattn_status_t make_plan(const pattn_problem_t* p, const void* q, const void* kc
   const bool q_ok = (p->q_stride_tok % 8 == 0) && (p->q_stride_head % 8 == 0) && (q == nullptr || aligned16(q));
   const bool o_ok = (p->o_stride_tok % 8 == 0) && (p->o_stride_head % 8 == 0) && (out == nullptr || aligned16(out));
   pl->use_k2 = bf16 && !generic && p->block_size % 16 == 0 && tma_ok && q_ok && o_ok;
+  // Block sizes that are not a multiple of 16 (no TMA box fits a page): decodes on K2W with
+  // cp.async-gathered entries when its other conditions hold (G <= 8, 2 | Hkv, 16-byte rows)
+  {
+    const int64_t e2 = 2;
+    const bool rows16 = (p->kv_stride_blk * e2) % 16 == 0 && (p->kv_stride_tok * e2) % 16 == 0 &&
+                        (p->kv_stride_head * e2) % 16 == 0 && (kc == nullptr || aligned16(kc)) &&
+                        (vc == nullptr || aligned16(vc));
+    pl->decode_gather = bf16 && !generic && p->block_size % 16 != 0 && rows16 && q_ok && o_ok &&
+                        pl->tuning.decode_kernel != 2 && wide_decode_heads(p->num_kv_heads, G) > 0;
+    if (pl->decode_gather) pl->use_k2 = true;
+  }
   if (p->flags & PATTN_FLAG_BASELINE) {  // the paper's baseline kernel alone (comparison only)
     pl->use_k7 = true;
     pl->use_k2 = false;
+    pl->decode_gather = false;
   }
 
   Params probe;
@@ -550,7 +564,10 @@ pattn_status_t run(const pattn_problem_t* p, const void* q, const void* k_cache,
   memset(&tmO, 0, sizeof(tmO));
   static thread_local KvHeadMaps head_maps;  // 16 KB: kept off the stack
   if (!metadata_only) {
-    if (pl.use_k2) {
+    if (pl.use_k2 && pl.decode_gather) {
+      memset(&tmK5, 0, sizeof(tmK5));  // K2W gathers its entries with cp.async: no tensor maps
+      memset(&tmV5, 0, sizeof(tmV5));
+    } else if (pl.use_k2) {
       const int hb = pl.decode_hb > 0 ? pl.decode_hb : 1;
       if (!encode_kv_map5(&tmK5, p, k_cache, hb) || !encode_kv_map5(&tmV5, p, v_cache, hb)) return PATTN_ERR_UNSUPPORTED;
     }

@@ -391,10 +391,12 @@ def test_segment_reduce_groups_follow_segment_count(flags):
 
 @pytest.mark.parametrize("dt,bs,layout", [("bf16", 7, "NHD"), ("f32", 16, "HND"), ("f32", 5, "NHD"), ("bf16", 24, "HND")])
 @pytest.mark.parametrize("flags", [0, 0x4])
-def test_split_decode_on_generic_path(dt, bs, layout, flags):
-    """Block sizes K2 cannot fetch (not a multiple of 16) and the fp32 path: decodes still run
-    as split-KV segments (parallel tiled softmax) -- on the SIMT kernel K4 -- and K3
-    merges them; long contexts get many segments."""
+def test_split_decode_on_generic_path(dt, bs, layout, flags, monkeypatch):
+    """Block sizes the TMA decode cannot fetch (not a multiple of 16) and the fp32 path: decodes
+    still run as split-KV segments (parallel tiled softmax) -- on the SIMT kernel K4
+    (bf16 here with the gathered K2W switched off: decode_kernel 2) -- and K3 merges them; long
+    contexts get many segments."""
+    monkeypatch.setenv("PATTN_DECODE_WIDE", "0")
     w = Workload("k4split", ((20000, 1), (0, 70), (3000, 1), (17, 1), (700, 40), (9000, 1)), 32, 8, 128, bs, dt)
     batch = generate(w, seed=17, dist="peaked", poison=True, layout=layout)
     db = DeviceBatch(batch)
@@ -690,4 +692,37 @@ def test_decode_wide_equals_narrow_needles(monkeypatch):
                     assert torch.equal(out[s, h], row), (wide, b, g, h, t)
         outs.append(out)
     assert torch.equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("heads,D,bs,dt,layout", [((32, 8), 128, 7, "bf16", "NHD"), ((64, 8), 128, 24, "bf16", "HND"),
+                                                  ((16, 2), 64, 5, "f16", "NHD"), ((28, 4), 128, 40, "bf16", "HND")])
+@pytest.mark.parametrize("flags", [0, 0x4])
+def test_gathered_decode_for_any_block_size(heads, D, bs, dt, layout, flags):
+    """Block sizes that are not a multiple of 16: K2W gathers its ring entries row by row with
+    cp.async (one block-table lookup per key, 16 keys spanning pages) -- planned as the decode
+    kernel, split into segments that end inside pages, merged by K3, matching the oracle."""
+    w = Workload("gather", ((20000, 1), (0, 70), (3000, 1), (17, 1), (700, 40), (9000, 1), (1, 1)), heads[0], heads[1],
+                 D, bs, dt)
+    batch = generate(w, seed=23 + bs, dist="peaked", poison=True, layout=layout)
+    db = DeviceBatch(batch)
+    p = P.make_problem(db.q, db.k, w.num_kv_heads, w.block_size, db.bt, w.num_seqs, None, layout, 70, 20001, flags)
+    assert P.planned_kernels(p) & (1 << P.KERNEL_DECODE) and P.planned_kernels(p) & P.PLAN_DECODE_WIDE
+    a = db.run(flags=flags).clone()
+    assert_close(out_f64(a), O.batch_attention(batch), dt, f"gathered K2W {heads} D{D} bs={bs} flags={flags}")
+    assert torch.equal(db.run(flags=flags), a)
+
+
+def test_gathered_decode_needles():
+    """Needle rows through the gathered K2W at bs 7: bit-exact V rows (paging arithmetic)."""
+    w = Workload("gneedle", tuple([(2999 + 5 * i, 1) for i in range(5)]), 32, 8, 128, 7, "bf16")
+    batch = generate(w, seed=71, dist="needle")
+    out = DeviceBatch(batch).run(flags=P.FLAG_FORCE_SPLIT).cpu()
+    v = O.widen(batch.v_cache)
+    for b in range(w.num_seqs):
+        s = int(batch.cu_seqlens_q[b])
+        for g in range(w.num_kv_heads):
+            t = int(batch.needle_pos[b, g])
+            row = torch.from_numpy(v[batch.block_table[b, t // 7], t % 7, g]).to(torch.bfloat16)
+            for h in range(g * 4, g * 4 + 4):
+                assert torch.equal(out[s, h], row), (b, g, h, t)
 
