@@ -271,6 +271,12 @@ PATTN_DEVICE void cp_async_16_hint(uint32_t dst, const void* src, uint64_t polic
   asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "l"(policy)
                : "memory");
 }
+// Same with a source size (0 -> the 16 destination bytes are zero-filled, nothing is read).
+PATTN_DEVICE void cp_async_16_zfill_hint(uint32_t dst, const void* src, int src_bytes, uint64_t policy) {
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;\n" ::"r"(dst), "l"(src),
+               "r"(src_bytes), "l"(policy)
+               : "memory");
+}
 // Arrive on `bar` once all of this thread's prior cp.async have completed; the arrival counts
 // against the barrier's initial count (noinc).
 PATTN_DEVICE void cp_async_mbar_arrive_noinc(uint64_t* bar) {

@@ -221,7 +221,12 @@ PATTN_DEVICE Item next_item(Bars& bar, const ItemSlot* ring, uint32_t n, int lan
   return x;
 }
 
-template <int D, typename E>
+// kGather: block sizes that are not a multiple of 16 (no 16-key TMA box fits a page): the four
+// producer warps gather each K / V tile row by row with 16-byte cp.async into the same swizzled
+// layout (one block-table lookup per key row; keys past the Q block's visible range zero-filled),
+// completing on the stage's mbarrier with cp.async.mbarrier.arrive.noinc (64 producer threads per
+// operand); everything else is unchanged.
+template <int D, typename E, bool kGather>
 __global__ void __launch_bounds__(kThreads, 1)
     k1_prefill(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmO,
                const __grid_constant__ KvHeadMaps maps, Params p) {
@@ -255,11 +260,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(&bar.q_full, 1);
     mbar_init(&bar.q_empty, kMmaWarps);
     for (int s = 0; s < kKStages; ++s) {
-      mbar_init(&bar.k_full[s], 1);
+      mbar_init(&bar.k_full[s], kGather ? 64 : 1);
       mbar_init(&bar.k_empty[s], kMmaWarps);
     }
     for (int s = 0; s < kVStages; ++s) {
-      mbar_init(&bar.v_full[s], 1);
+      mbar_init(&bar.v_full[s], kGather ? 64 : 1);
       mbar_init(&bar.v_empty[s], kMmaWarps);
     }
     for (int h = 0; h < 2; ++h) {
@@ -311,6 +316,39 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint64_t pol_kv = l2_policy_evict_last();  // K/V tiles are re-read by the sequence's other Q blocks
     const int nst = kv ? kVStages : kKStages;
     uint32_t ic = 0, cnt = 0;
+    if constexpr (kGather) {
+      static_assert(kN == 64, "one key row per producer thread");
+      const int t = (owner ? 0 : 32) + lane;  // this thread's key row of every tile
+      constexpr int esz = (int)sizeof(typename E::T);
+      for (;; ++ic) {
+        const Item x = next_item(bar, ring, ic, lane);
+        if (x.ntiles < 0) break;
+        const uint8_t* gbase = static_cast<const uint8_t*>(kv ? p.v : p.k) + (int64_t)x.kvh * p.kv_st_head * esz;
+        const int32_t* bt = p.block_table + (int64_t)x.b * p.bt_stride;
+        for (int jt = 0; jt < x.ntiles; ++jt) {
+          const uint32_t s = cnt % nst, ph = (cnt / nst) & 1u;
+          uint64_t* fullb = kv ? &bar.v_full[s] : &bar.k_full[s];
+          uint64_t* emptyb = kv ? &bar.v_empty[s] : &bar.k_empty[s];
+          const uint32_t dst = smem_u32(smem + (kv ? kOffV : kOffK) + s * kTile) + (t >> 3) * kGroup + (t & 7) * 128;
+          const int key = jt * kN + t;
+          const uint8_t* src = gbase;
+          int bytes = 0;  // 0: zero-fill (keys past the visible range, and past the sequence end)
+          if (key < x.kv_end) {
+            const int pg = key / p.bs;
+            src = gbase + ((int64_t)__ldg(bt + pg) * p.kv_st_blk + (int64_t)(key - pg * p.bs) * p.kv_st_tok) * esz;
+            bytes = 16;
+          }
+          if (lane == 0) mbar_wait(emptyb, ph ^ 1u);
+          __syncwarp();
+#pragma unroll
+          for (int c = 0; c < D / 8; ++c)  // 16-byte chunk c of the row: d half c / 8, chunk c % 8 (swizzled)
+            cp_async_16_zfill_hint(dst + (c >> 3) * 1024 + (((c & 7) ^ (t & 7)) << 4), src + (bytes ? c * 16 : 0),
+                                   bytes, pol_kv);
+          cp_async_mbar_arrive_noinc(fullb);
+          ++cnt;
+        }
+      }
+    } else
     for (;; ++ic) {
       int id0;
       const Item x = next_item(bar, ring, ic, lane, &id0);
@@ -449,8 +487,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (it < n_items) {
           const Item x = prefill_item(p, total_qb, it, lane);
           const int nsb_valid = (x.kv_end + 15) / 16;
-          const int id = (lane < 8 && lane < nsb_valid) ? __ldg(p.block_table + (int64_t)x.b * p.bt_stride + lane / n16)
-                                                        : p.num_blocks;
+          // (gathered producers look their rows up themselves: no prefetch, and n16 = 0 there)
+          const int id = (!kGather && lane < 8 && lane < nsb_valid)
+                             ? __ldg(p.block_table + (int64_t)x.b * p.bt_stride + lane / n16)
+                             : p.num_blocks;
           int ids[8];
 #pragma unroll
           for (int q = 0; q < 8; ++q) ids[q] = __shfl_sync(0xffffffffu, id, q);
@@ -716,8 +756,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 bool prefill_supported(const Params& p) {
   if (getenv("PATTN_DISABLE_K1")) return false;
   // BLOCK_Q = 2 * floor(128 / G) tokens in two halves of 128 rows (padding rows when G does not
-  // divide 128, e.g. G = 3, 5, 6, 7, 12); head_dim 64 or 128
-  return (p.D == 64 || p.D == 128) && p.G >= 1 && p.G <= 64 && p.bs % 16 == 0 &&
+  // divide 128, e.g. G = 3, 5, 6, 7, 12); head_dim 64 or 128; block sizes that are not a
+  // multiple of 16 take the gathered producers (16-byte aligned K/V rows)
+  return (p.D == 64 || p.D == 128) && p.G >= 1 && p.G <= 64 && (p.bs % 16 == 0 || p.kv_vec16) &&
          p.Hkv <= kMaxKvHeadMaps;
 }
 
@@ -730,13 +771,20 @@ PrefillLaunch plan_prefill(const Params& p, int num_sms) {
   return pl;
 }
 
-cudaError_t launch_prefill(const Params& p, const PrefillLaunch& pl, const CUtensorMap& tmQ, const CUtensorMap& tmO,
-                           const KvHeadMaps& kv, cudaStream_t stream) {
-  auto kern = p.dtype == 2 ? (p.D == 64 ? k1_prefill<64, EltF16> : k1_prefill<128, EltF16>)
-                           : (p.D == 64 ? k1_prefill<64, EltBf16> : k1_prefill<128, EltBf16>);
+template <bool G>
+static cudaError_t launch_prefill_g(const Params& p, const PrefillLaunch& pl, const CUtensorMap& tmQ,
+                                    const CUtensorMap& tmO, const KvHeadMaps& kv, cudaStream_t stream) {
+  auto kern = p.dtype == 2 ? (p.D == 64 ? k1_prefill<64, EltF16, G> : k1_prefill<128, EltF16, G>)
+                           : (p.D == 64 ? k1_prefill<64, EltBf16, G> : k1_prefill<128, EltBf16, G>);
   cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(kern), pl.smem);
   if (e != cudaSuccess) return e;
   return launch_pdl(kern, dim3(pl.grid), dim3(kThreads), pl.smem, stream, tmQ, tmO, kv, p);
+}
+
+cudaError_t launch_prefill(const Params& p, const PrefillLaunch& pl, const CUtensorMap& tmQ, const CUtensorMap& tmO,
+                           const KvHeadMaps& kv, cudaStream_t stream) {
+  return p.bs % 16 == 0 ? launch_prefill_g<false>(p, pl, tmQ, tmO, kv, stream)
+                        : launch_prefill_g<true>(p, pl, tmQ, tmO, kv, stream);
 }
 
 }  // namespace pattn

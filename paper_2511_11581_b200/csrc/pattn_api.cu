@@ -280,6 +280,11 @@ pattn_status_t make_plan(const pattn_problem_t* p, const void* q, const void* kc
     pl->decode_gather = false;
   }
 
+  // 16-byte aligned K/V rows: K4's vector loads, and the gathered K1 / K2W producers
+  const int64_t esz = bf16 ? 2 : 4;
+  pl->kv_vec16 = (p->kv_stride_blk * esz) % 16 == 0 && (p->kv_stride_tok * esz) % 16 == 0 &&
+                 (p->kv_stride_head * esz) % 16 == 0 && (D * esz) % 16 == 0 && (kc == nullptr || aligned16(kc)) &&
+                 (vc == nullptr || aligned16(vc));
   Params probe;
   fill_params(p, *pl, &probe);
   pl->use_k1 = bf16 && !generic && !pl->use_k7 && tma_ok && q_ok && o_ok && prefill_supported(probe);
@@ -295,13 +300,9 @@ pattn_status_t make_plan(const pattn_problem_t* p, const void* q, const void* kc
   // No K2 (fp32, block sizes that are not a multiple of 16, unaligned strides): K4 runs the
   // decodes as split-KV segment units too (parallel tiled softmax on the SIMT path), merged by K3
   // (K3 stores 16-byte vectors: output rows must be 16-byte aligned, else decodes stay unsplit)
-  const int64_t esz = bf16 ? 2 : 4;
   const bool o_vec = (p->o_stride_tok * esz) % 16 == 0 && (p->o_stride_head * esz) % 16 == 0 &&
                      (out == nullptr || aligned16(out));
   pl->k4_decodes = !pl->use_k2 && !pl->use_k7 && o_vec;
-  pl->kv_vec16 = (p->kv_stride_blk * esz) % 16 == 0 && (p->kv_stride_tok * esz) % 16 == 0 &&
-                 (p->kv_stride_head * esz) % 16 == 0 && (D * esz) % 16 == 0 && (kc == nullptr || aligned16(kc)) &&
-                 (vc == nullptr || aligned16(vc));
   if (pl->k4_decodes) pl->use_k4 = true;
   const int bm = pl->block_q * G;
   pl->rpw = bm <= 32 ? 8 : 16;
@@ -571,7 +572,7 @@ pattn_status_t run(const pattn_problem_t* p, const void* q, const void* k_cache,
       const int hb = pl.decode_hb > 0 ? pl.decode_hb : 1;
       if (!encode_kv_map5(&tmK5, p, k_cache, hb) || !encode_kv_map5(&tmV5, p, v_cache, hb)) return PATTN_ERR_UNSUPPORTED;
     }
-    if (pl.use_k1) {
+    if (pl.use_k1 && p->block_size % 16 == 0) {  // (other block sizes: K1 gathers rows with cp.async)
       if (!encode_head_maps(&head_maps, p, k_cache, v_cache)) return PATTN_ERR_UNSUPPORTED;
     }
     if (pl.use_k1) {

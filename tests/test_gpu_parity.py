@@ -397,6 +397,7 @@ def test_split_decode_on_generic_path(dt, bs, layout, flags, monkeypatch):
     (bf16 here with the gathered K2W switched off: decode_kernel 2) -- and K3 merges them; long
     contexts get many segments."""
     monkeypatch.setenv("PATTN_DECODE_WIDE", "0")
+    monkeypatch.setenv("PATTN_DISABLE_K1", "1")  # the prefills too (K1 gathers rows for such block sizes)
     w = Workload("k4split", ((20000, 1), (0, 70), (3000, 1), (17, 1), (700, 40), (9000, 1)), 32, 8, 128, bs, dt)
     batch = generate(w, seed=17, dist="peaked", poison=True, layout=layout)
     db = DeviceBatch(batch)
@@ -725,4 +726,21 @@ def test_gathered_decode_needles():
             row = torch.from_numpy(v[batch.block_table[b, t // 7], t % 7, g]).to(torch.bfloat16)
             for h in range(g * 4, g * 4 + 4):
                 assert torch.equal(out[s, h], row), (b, g, h, t)
+
+
+@pytest.mark.parametrize("heads,D,bs,dt,layout", [((32, 8), 128, 7, "bf16", "NHD"), ((64, 8), 128, 24, "bf16", "HND"),
+                                                  ((8, 8), 64, 5, "f16", "NHD"), ((28, 4), 128, 40, "bf16", "HND"),
+                                                  ((96, 8), 128, 12, "bf16", "NHD")])
+def test_gathered_prefill_for_any_block_size(heads, D, bs, dt, layout):
+    """Block sizes that are not a multiple of 16 on the tensor-core prefill: K1's producers gather
+    each 64-key tile row by row with cp.async (keys past the visible range zero-filled) --
+    planned, matching the oracle on prefills with and without context, ragged tails."""
+    w = Workload("gpre", ((0, 333), (500, 130), (3, 1), (61, 200), (1000, 1), (0, 17)), heads[0], heads[1], D, bs, dt)
+    batch = generate(w, seed=31 + bs, dist="peaked", poison=True, layout=layout)
+    db = DeviceBatch(batch)
+    p = P.make_problem(db.q, db.k, w.num_kv_heads, w.block_size, db.bt, w.num_seqs, None, layout, 333, 1000)
+    assert P.planned_kernels(p) & (1 << P.KERNEL_PREFILL)
+    a = db.run().clone()
+    assert_close(out_f64(a), O.batch_attention(batch), dt, f"gathered K1 {heads} D{D} bs={bs}")
+    assert torch.equal(db.run(), a)
 

@@ -131,8 +131,10 @@ ATTRIBUTION: Dict[str, Workload] = {
     "x_g7_mixed": Workload("x_g7_mixed", tuple([(0, 2048)] * 8 + [(4096, 1)] * 56), 28, 4, 128, 16, "bf16"),
     # head_dim 64 (32 / 8 heads): the D = 64 instantiation of the tcgen05 prefill kernel
     "x_d64_mixed": Workload("x_d64_mixed", tuple([(0, 2048)] * 8 + [(4096, 1)] * 56), 32, 8, 64, 16, "bf16"),
-    # block size 7 (not a multiple of 16): long decodes split on the SIMT kernel, merged by K3
+    # block size 7 (not a multiple of 16): long decodes split on K2W with cp.async-gathered rows, merged by K3
     "x_bs7_decode32k": Workload("x_bs7_decode32k", tuple((32768, 1) for _ in range(8)), 32, 8, 128, 7, "bf16"),
+    # config 3's mix with block size 7: K1 and K2W gather K/V rows with cp.async (no TMA box fits a page)
+    "x_bs7_mixed": Workload("x_bs7_mixed", tuple([(0, 2048)] * 8 + [(4096, 1)] * 56), 32, 8, 128, 7, "bf16"),
 }
 
 
