@@ -315,10 +315,12 @@ def _sample_rows(batch, n_random, rng):
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("name", ["c2_decode8b", "c3_mixed8b", "c4_decode128k", "c5_mixed70b"])
+@pytest.mark.parametrize("name", ["c2_decode8b", "c3_mixed8b", "c4_decode128k", "c5_mixed70b", "x_bs7_mixed"])
 def test_full_size_sampled(name):
-    w = CONFIGS[name]
-    batch = generate(w, seed=2000 + list(CONFIGS).index(name), dist="peaked", poison=True)
+    from workloads.gen import ATTRIBUTION
+
+    w = CONFIGS[name] if name in CONFIGS else ATTRIBUTION[name]
+    batch = generate(w, seed=2000 + (list(CONFIGS) + list(ATTRIBUTION)).index(name), dist="peaked", poison=True)
     db = DeviceBatch(batch)
     o_serial = db.run()
     if any(q > 1 for _, q in w.seqs):
