@@ -13,17 +13,19 @@
 //   work item = (decode segment c, group of HB KV heads); K5 plans segments with Hkv / HB
 //     items per segment (units per segment, Params::decode_hb).
 //   warp 0 (producer): per 16-key sub-block of the segment, ONE K box and ONE V box
-//     {64 d, 16 slots, D/64 halves, HB heads, 1 block} into a ring stage (they land as HB
-//     head-major copies of K2's [half][slot][64 d] layout, 128B-swizzled).
-//   warps 1..HB (consumers): warp w owns KV head hb*HB + w for the whole item -- every stage,
-//     in key order -- with its G <= 8 query heads as the N = 8 columns of mma.sync (S^T =
-//     K.Q^T, O^T = V^T.P^T, online softmax in the log2 domain, exactly K2's per-stage math).
-//     A stage is released when all HB warps have consumed it.  No cross-warp merge: each warp
-//     writes its head's output (single-segment sequences) or (m, l, acc) partial for K3
-//     straight from its mma fragments.
-// Requirements (planner): G <= 8 (one head group), HB in {2, 4, 8} dividing Hkv, block size a
-// multiple of 16, 16-byte aligned K/V rows (TMA).  V slots past the sequence end are zeroed in
-// shared memory before PV (they may hold NaN; reading R13), scores there are masked by select.
+//     {64 d, 16 slots, D/64 halves, HB heads, 1 block} into two consecutive entries of a ring
+//     of single-operand entries (each lands as HB head-major copies of K2's [half][slot][64 d]
+//     layout, 128B-swizzled).  Block sizes that are not a multiple of 16 (kGather): four
+//     producer warps fill the same entries row by row with cp.async instead.
+//   warps (consumers): warp w owns KV head hb*HB + w for the whole item -- every sub-block, in
+//     key order -- with its G <= 8 query heads as the N = 8 columns of mma.sync (S^T = K.Q^T,
+//     O^T = V^T.P^T, online softmax in the log2 domain with a lazy running max).  An entry is
+//     released when all HB warps have consumed it: K(j) right after the scores, V(j) after PV.
+//     No cross-warp merge: each warp writes its head's output (single-segment sequences) or
+//     (m, l, acc) partial for K3 straight from its mma fragments.
+// Requirements (planner): G <= 8 (one head group), HB in {2, 4, 8} dividing Hkv, 16-byte aligned
+// K/V rows.  V rows past the segment's keys are zeroed in shared memory before PV (slots past
+// the sequence end may hold NaN; reading R13), scores there are masked by select.
 #include <algorithm>
 #include <cstdlib>
 
