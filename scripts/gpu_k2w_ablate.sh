@@ -1,12 +1,12 @@
 #!/bin/bash
-# K2W per-SM rate on 36 SMs (full kernel / no-load ablation) and configs 2-5.
+# K2W per-SM rate on 36 SMs and configs 2-4 / mixed 3.  (The no-load / no-compute ablations of
+# DESIGN.md §6 K2W were variants built from patches with -DPATTN_K2W_NOLOAD / NOCOMPUTE, since removed.)
 one() { python -c "
 import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); t=d['kernel_ms']['decode']
 print('$1', 'decode', round(t*1e3,1), 'us', round(0.9407/t/36*1e3,1), 'GB/s/SM')"; }
 run() { PATTN_DECODE_SMS=36 timeout 120 python bench.py --workload c3d_decode_part --streams 1 --steps 30 --warmup 5 --no-cpu-baseline --no-e2e --no-sub 2>/dev/null | one "$1"; }
 [ -n "$TESTS" ] && timeout 600 python -m pytest tests/test_gpu_parity.py -q -x -k "$TESTS" 2>&1 | tail -2
 run main
-PATTN_LIB=$PWD/variants/k2w_noload/libpattn.so run noload
 two() { python -c "
 import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1])
 r=d['roofline_kernels']
