@@ -746,3 +746,32 @@ def test_gathered_prefill_for_any_block_size(heads, D, bs, dt, layout):
     assert_close(out_f64(a), O.batch_attention(batch), dt, f"gathered K1 {heads} D{D} bs={bs}")
     assert torch.equal(db.run(), a)
 
+
+
+def test_large_batch_multi_pass_metadata():
+    """More sequences than K5's 1024 threads (its multi-pass scan), decodes on K2W and K3,
+    prefills on K1, empty sequences in between: plan bit-exact vs the oracle's metadata and the
+    output vs the oracle."""
+    rng = np.random.default_rng(1500)
+    seqs = []
+    for i in range(1500):
+        u = rng.random()
+        if u < 0.9:
+            seqs.append((int(rng.integers(1, 700)), 1))
+        elif u < 0.97:
+            seqs.append((int(rng.integers(0, 200)), int(rng.integers(2, 90))))
+        else:
+            seqs.append((0, 0))
+    w = Workload("bigB", tuple(seqs), 32, 8, 128, 16, "bf16")
+    batch = generate(w, seed=1500, dist="peaked", poison=True)
+    db = DeviceBatch(batch)
+    prob = P.make_problem(db.q, db.k, w.num_kv_heads, w.block_size, db.bt, w.num_seqs)
+    plan = P.debug_plan(prob, db.cu, db.sl).cpu().numpy()
+    B = w.num_seqs
+    qlens = np.diff(batch.cu_seqlens_q)
+    dec = qlens == 1
+    cu_qb_ref = M.build_batch_meta(np.concatenate([[0], np.cumsum(np.where(dec, 0, qlens))]),
+                                   np.where(dec, 0, batch.seq_lens), int(plan[3]))["cu_q_blocks"]
+    assert plan[8:8 + B + 1].tolist() == cu_qb_ref.tolist()
+    assert plan[1] == int(dec.sum())
+    _check(batch, 0, "1500 sequences")
