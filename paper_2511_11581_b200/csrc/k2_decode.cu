@@ -254,12 +254,14 @@ __global__ void __launch_bounds__((NCW + kNP) * 32, 1)
     // complete out of order: a waiter must have observed phase u-1 of a stage before it
     // waits on phase u, otherwise the parity test aliases and returns early.)  Items start
     // at g % NCW == 0 (the producer pads with empty stages), so warp cw takes j = cw mod NCW.
-    // S^T[16 keys x 8 heads] = K . Q^T of sub-block jj (waits for its stage)
-    auto scores = [&](int jj, float (&sc)[4]) {
+    // This warp's ring position, kept incrementally (one division per item instead of one per
+    // stage: nst is a runtime value; it is a multiple of NCW, so stepping by NCW wraps cleanly).
+    uint32_t ws = (g + cw) % nst, wph = ((g + cw) / nst) & 1u;
+    // S^T[16 keys x 8 heads] = K . Q^T of sub-block jj (waits for its stage sq, phase sph)
+    auto scores = [&](int jj, uint32_t sq, uint32_t sph, float (&sc)[4]) {
       const uint32_t gq = g + jj;
-      const uint32_t sq = gq % nst;
       if (lane == 0) PATTN_EV(k2, 1, gq);
-      mbar_wait_tag(&full[sq], (gq / nst) & 1u, (int)gq, it, jj);
+      mbar_wait_tag(&full[sq], sph, (int)gq, it, jj);
       if (lane == 0) PATTN_EV(k2, 2, gq);
       const uint32_t kq = ring_u32 + sq * S::kStageBytes;
       sc[0] = sc[1] = sc[2] = sc[3] = 0.f;
@@ -275,9 +277,11 @@ __global__ void __launch_bounds__((NCW + kNP) * 32, 1)
     };
     for (int j = cw; j < nsb; j += NCW) {
       const uint32_t gg = g + j;
-      const uint32_t s = gg % nst;
+      const uint32_t s = ws;
       float sc[4];
-      scores(j, sc);
+      scores(j, ws, wph, sc);
+      ws += NCW;
+      if (ws >= (uint32_t)nst) ws -= (uint32_t)nst, wph ^= 1u;
       const uint32_t kst = ring_u32 + s * S::kStageBytes;
       const uint32_t vst = kst + S::kOpBytes;
       const int valid = x.L - (x.sb0 + j) * kSub;  // slots [0, valid) hold real keys

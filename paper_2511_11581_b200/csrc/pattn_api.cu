@@ -139,7 +139,8 @@ double feature_value(const pattn_problem_t* p, int f) {
 }
 
 // Tree leaf for p (all zero when no tree is loaded), then env overrides, then defaults.
-pattn_tuning_t resolve_tuning(const pattn_problem_t* p) {
+// *leaf_kernel: the decode kernel the leaf's decode knobs were measured with (before overrides).
+pattn_tuning_t resolve_tuning(const pattn_problem_t* p, int* leaf_kernel = nullptr) {
   pattn_tuning_t t{0, 0, 0, 0, 0, 0};
   {
     TuningTree& tt = tuning_tree();
@@ -153,6 +154,7 @@ pattn_tuning_t resolve_tuning(const pattn_problem_t* p) {
       t = tt.nodes[i].leaf;
     }
   }
+  if (leaf_kernel) *leaf_kernel = t.decode_kernel == 2 ? 2 : 1;
   const char* e;
   if ((e = getenv("PATTN_ITEMS_PER_SM")) && *e) t.items_per_sm = atoi(e);
   if ((e = getenv("PATTN_MIN_CHUNK_TOKENS")) && *e) t.min_chunk_tokens = atoi(e);
@@ -174,6 +176,8 @@ struct Plan {
   bool kv_vec16 = false;    // K/V rows 16-byte aligned (K4 vector loads)
   int block_q = 1, HG = 1, rpw = 8;
   int decode_hb = 0;  // > 0: decodes on K2W (head-wide boxes)
+  int leaf_kernel = 1;  // the decode kernel the tuning leaf's decode knobs were measured with
+  int decode_ctas = 2;  // K2 CTAs per SM
   bool decode_gather = false;  // K2W with cp.async-gathered entries (block size not a multiple of 16)
   int target_items = 0, min_chunk = 1, split_mode = 0, max_chunks = 0;
   int num_sms = 148;
@@ -246,7 +250,7 @@ pattn_status_t make_plan(const pattn_problem_t* p, const void* q, const void* kc
   pattn_status_t st = check_problem(p);
   if (st != PATTN_OK) return st;
   DeviceInfo di = device_info();
-  pl->tuning = resolve_tuning(p);
+  pl->tuning = resolve_tuning(p, &pl->leaf_kernel);
   pl->num_sms = di.ok ? di.sms : 148;
   pl->max_smem = di.ok ? di.max_smem : 227 * 1024;
   const int G = p->num_q_heads / p->num_kv_heads;
@@ -316,9 +320,18 @@ pattn_status_t make_plan(const pattn_problem_t* p, const void* q, const void* kc
   // whose items are HB x larger, 2 and 128 (the tuning sweep's best single configuration,
   // profiles/r02/tuning_holdout.json; more segments cost K3 partial traffic: config 4 at 32 per SM
   // wrote 153 MB of partials).
-  const bool leaf_fits = (pl->decode_hb > 0) == (pl->tuning.decode_kernel != 2);
-  const int items_per_sm = leaf_fits && pl->tuning.items_per_sm > 0 ? pl->tuning.items_per_sm : (pl->decode_hb ? 2 : 16);
-  const int min_tok = leaf_fits && pl->tuning.min_chunk_tokens > 0 ? pl->tuning.min_chunk_tokens : (pl->decode_hb ? 128 : 256);
+  // (environment overrides always apply)
+  const bool leaf_fits = (pl->decode_hb > 0) == (pl->leaf_kernel == 1);
+  auto env_set = [](const char* n) {
+    const char* v = getenv(n);
+    return v && *v;
+  };
+  const bool use_items = (leaf_fits || env_set("PATTN_ITEMS_PER_SM")) && pl->tuning.items_per_sm > 0;
+  const bool use_min = (leaf_fits || env_set("PATTN_MIN_CHUNK_TOKENS")) && pl->tuning.min_chunk_tokens > 0;
+  const bool use_ctas = leaf_fits || env_set("PATTN_DECODE_CTAS");
+  const int items_per_sm = use_items ? pl->tuning.items_per_sm : (pl->decode_hb ? 2 : 16);
+  const int min_tok = use_min ? pl->tuning.min_chunk_tokens : (pl->decode_hb ? 128 : 256);
+  pl->decode_ctas = use_ctas ? pl->tuning.decode_ctas_per_sm : 2;
   if (p->flags & PATTN_FLAG_NO_SPLIT) {
     pl->split_mode = 1;
     pl->target_items = 1;
@@ -368,7 +381,7 @@ pattn_status_t make_plan(const pattn_problem_t* p, const void* q, const void* kc
   fill_params(p, *pl, &probe);
   if (pl->use_k2)
     pl->dl = pl->decode_hb ? plan_decode_wide(probe, pl->num_sms, pl->max_smem)
-                           : plan_decode(probe, pl->num_sms, pl->max_smem, pl->tuning.decode_ctas_per_sm);
+                           : plan_decode(probe, pl->num_sms, pl->max_smem, pl->decode_ctas);
   if (pl->use_k1) pl->pl = plan_prefill(probe, pl->num_sms);
   return PATTN_OK;
 }
