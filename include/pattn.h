@@ -238,7 +238,7 @@ typedef struct pattn_tuning {
                                  (default: the measured rate of the decode kernel in use, K2W 80000, K2 61000) */
   int32_t serial;             /* mixed batches: 1 = prefill and decode kernels back to back on one stream
                                  even when a second stream is given; 0 = concurrent (default) */
-  int32_t decode_kernel;      /* decode kernel: 1 = K2W (head-wide TMA boxes) where it applies (G <= 8,
+  int32_t decode_kernel;      /* decode kernel: 1 = K2W (head-wide TMA boxes) where it applies (G <= 16,
                                  2 | Hkv), 2 = K2 (one KV head per work item); default 1 */
 } pattn_tuning_t;           /* 0 in a field = built-in default */
 

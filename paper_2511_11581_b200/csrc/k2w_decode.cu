@@ -23,7 +23,8 @@
 //     released when all HB warps have consumed it: K(j) right after the scores, V(j) after PV.
 //     No cross-warp merge: each warp writes its head's output (single-segment sequences) or
 //     (m, l, acc) partial for K3 straight from its mma fragments.
-// Requirements (planner): G <= 8 (one head group), HB in {2, 4, 8} dividing Hkv, 16-byte aligned
+// Requirements (planner): G <= 16 (one or two head groups of <= 8 query heads: one consumer warp
+// per (KV head, head group)), HB in {2, 4, 8} dividing Hkv, 16-byte aligned
 // K/V rows.  V rows past the segment's keys are zeroed in shared memory before PV (slots past
 // the sequence end may hold NaN; reading R13), scores there are masked by select.
 #include <algorithm>
@@ -80,8 +81,10 @@ __device__ __forceinline__ WItem wide_item(const Params& p, int it, int ngroups)
 // warps gather the same ring entries row by row with 16-byte cp.async (one block-table lookup per
 // key row, any block size, 16-byte aligned rows), completing on the entry's mbarrier through
 // cp.async.mbarrier.arrive.noinc; the consumers are unchanged.
-template <int D, int HB, typename E, bool kGather>
-__global__ void __launch_bounds__((HB + (kGather ? 4 : 1)) * 32, 1)
+// HGW: head groups of <= 8 query heads per KV head (G <= 8: 1; 8 < G <= 16: 2); the consumer
+// warps are (KV head, head group) pairs.
+template <int D, int HB, typename E, bool kGather, int HGW>
+__global__ void __launch_bounds__((HB * HGW + (kGather ? 4 : 1)) * 32, 1)
     k2w_decode(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, Params p,
                int nent) {
   using S = WideShape<D, HB>;
@@ -114,11 +117,11 @@ __global__ void __launch_bounds__((HB + (kGather ? 4 : 1)) * 32, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < nent; ++s) {
       mbar_init(&full[s], kGather ? kProd * 32 : 1);  // gather: one noinc arrive per producer thread
-      mbar_init(&empty[s], HB);
+      mbar_init(&empty[s], HB * HGW);
     }
     for (int i = 0; i < kItemRing; ++i) {
       mbar_init(&item_full[i], 1);
-      mbar_init(&item_empty[i], HB + kProd - 1);  // consumers + the other producer warps
+      mbar_init(&item_empty[i], HB * HGW + kProd - 1);  // consumers + the other producer warps
     }
     fence_barrier_init();
   }
@@ -240,7 +243,7 @@ __global__ void __launch_bounds__((HB + (kGather ? 4 : 1)) * 32, 1)
   }
 
   // -------------------------------------------------------------- consumers (one KV head each)
-  const int w = warp - kProd;
+  const int w = (warp - kProd) / HGW, hg = (warp - kProd) % HGW;  // KV head (in the box), head group
   const int r = lane >> 2, c = lane & 3;       // mma fragment coordinates
   const int mat = lane >> 3, mrow = lane & 7;  // ldmatrix source coordinates
   using ET = typename E::T;
@@ -258,7 +261,8 @@ __global__ void __launch_bounds__((HB + (kGather ? 4 : 1)) * 32, 1)
     if (it >= n_items) break;
     const WItem x = wide_item(p, it, ngroups);
     const int kvh = x.hb * HB + w;
-    const int head0 = kvh * G;
+    const int head0 = kvh * G + hg * 8;
+    const int ge = min(8, G - hg * 8);  // query heads of this warp's group
 
     // Q^T as the B operand of S^T = K . Q^T: b0 = Q[head r][16kc + 2c .. +1], b1 = +8
     uint32_t bq[S::kKC][2];
@@ -266,8 +270,8 @@ __global__ void __launch_bounds__((HB + (kGather ? 4 : 1)) * 32, 1)
       const ET* qrow = Q + (int64_t)x.tok * p.q_st_tok + (int64_t)(head0 + r) * p.q_st_head;
 #pragma unroll
       for (int kc = 0; kc < S::kKC; ++kc) {
-        bq[kc][0] = r < G ? __ldg(reinterpret_cast<const uint32_t*>(qrow + kc * 16 + 2 * c)) : 0u;
-        bq[kc][1] = r < G ? __ldg(reinterpret_cast<const uint32_t*>(qrow + kc * 16 + 2 * c + 8)) : 0u;
+        bq[kc][0] = r < ge ? __ldg(reinterpret_cast<const uint32_t*>(qrow + kc * 16 + 2 * c)) : 0u;
+        bq[kc][1] = r < ge ? __ldg(reinterpret_cast<const uint32_t*>(qrow + kc * 16 + 2 * c + 8)) : 0u;
       }
     }
     float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
@@ -377,7 +381,7 @@ __global__ void __launch_bounds__((HB + (kGather ? 4 : 1)) * 32, 1)
       l0 += __shfl_xor_sync(0xffffffffu, l0, o);
       l1 += __shfl_xor_sync(0xffffffffu, l1, o);
     }
-    const bool h0ok = 2 * c < G, h1ok = 2 * c + 1 < G;
+    const bool h0ok = 2 * c < ge, h1ok = 2 * c + 1 < ge;
     if (x.nseg == 1) {
       const float i0 = 1.f / l0, i1 = 1.f / l1;
       ET* o0 = O + (int64_t)x.tok * p.o_st_tok + (int64_t)(head0 + 2 * c) * p.o_st_head;
@@ -422,19 +426,23 @@ __global__ void __launch_bounds__((HB + (kGather ? 4 : 1)) * 32, 1)
   }
 }
 
-template <int D, int HB, typename E, bool G>
+template <int D, int HB, typename E, bool G, int HGW>
 cudaError_t launch_wg(const Params& p, const DecodeLaunch& dl, const CUtensorMap& tmK, const CUtensorMap& tmV,
                       cudaStream_t stream) {
-  auto kern = k2w_decode<D, HB, E, G>;
+  auto kern = k2w_decode<D, HB, E, G, HGW>;
   cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(kern), dl.smem);
   if (e != cudaSuccess) return e;
-  return launch_pdl(kern, dim3(dl.grid), dim3((HB + (G ? 4 : 1)) * 32), dl.smem, stream, tmK, tmV, p, dl.stages);
+  return launch_pdl(kern, dim3(dl.grid), dim3((HB * HGW + (G ? 4 : 1)) * 32), dl.smem, stream, tmK, tmV, p,
+                    dl.stages);
 }
 template <int D, int HB, typename E>
 cudaError_t launch_w(const Params& p, const DecodeLaunch& dl, const CUtensorMap& tmK, const CUtensorMap& tmV,
                      cudaStream_t stream) {
-  return p.decode_gather ? launch_wg<D, HB, E, true>(p, dl, tmK, tmV, stream)
-                         : launch_wg<D, HB, E, false>(p, dl, tmK, tmV, stream);
+  if (p.G > 8)
+    return p.decode_gather ? launch_wg<D, HB, E, true, 2>(p, dl, tmK, tmV, stream)
+                           : launch_wg<D, HB, E, false, 2>(p, dl, tmK, tmV, stream);
+  return p.decode_gather ? launch_wg<D, HB, E, true, 1>(p, dl, tmK, tmV, stream)
+                         : launch_wg<D, HB, E, false, 1>(p, dl, tmK, tmV, stream);
 }
 
 template <int D, typename E>
@@ -451,7 +459,7 @@ cudaError_t launch_wd(const Params& p, const DecodeLaunch& dl, const CUtensorMap
 }  // namespace
 
 int wide_decode_heads(int Hkv, int G) {
-  if (G > 8) return 0;
+  if (G > 16) return 0;  // G <= 16: one or two head groups of <= 8 query heads per KV head
   const char* e = getenv("PATTN_DECODE_WIDE_HB");  // sweeps: cap on heads per box
   int cap = (e && *e) ? atoi(e) : 8;
   for (int hb = 8; hb >= 2; hb >>= 1)
@@ -463,7 +471,7 @@ int wide_decode_heads(int Hkv, int G) {
 // 2 x 16 x HB x D x 2 B stage.
 DecodeLaunch plan_decode_wide(const Params& p, int num_sms, size_t max_smem) {
   DecodeLaunch dl;
-  dl.consumer_warps = p.decode_hb;
+  dl.consumer_warps = p.decode_hb * (p.G > 8 ? 2 : 1);
   const size_t entry = (size_t)kSub * p.decode_hb * p.D * 2;  // one operand box
   const size_t fixed = 1024 /*align slack*/ + 2 * kItemRing * sizeof(uint64_t) + kItemRing * sizeof(int) + 64;
   const size_t cap = (max_smem < 227 * 1024 ? max_smem : 227 * 1024);

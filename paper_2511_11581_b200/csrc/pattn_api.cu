@@ -268,7 +268,7 @@ pattn_status_t make_plan(const pattn_problem_t* p, const void* q, const void* kc
   const bool o_ok = (p->o_stride_tok % 8 == 0) && (p->o_stride_head % 8 == 0) && (out == nullptr || aligned16(out));
   pl->use_k2 = bf16 && !generic && p->block_size % 16 == 0 && tma_ok && q_ok && o_ok;
   // Block sizes that are not a multiple of 16 (no TMA box fits a page): decodes on K2W with
-  // cp.async-gathered entries when its other conditions hold (G <= 8, 2 | Hkv, 16-byte rows)
+  // cp.async-gathered entries when its other conditions hold (G <= 16, 2 | Hkv, 16-byte rows)
   {
     const int64_t e2 = 2;
     const bool rows16 = (p->kv_stride_blk * e2) % 16 == 0 && (p->kv_stride_tok * e2) % 16 == 0 &&
@@ -312,7 +312,7 @@ pattn_status_t make_plan(const pattn_problem_t* p, const void* q, const void* kc
   pl->rpw = bm <= 32 ? 8 : 16;
 
   // Decode kernel.  K2W: decode items of HB KV heads (one TMA request per 16 keys x HB heads;
-  // default whenever G <= 8 and 2 | Hkv, tuning decode_kernel 2 / PATTN_DECODE_WIDE=0 keeps K2).
+  // default whenever G <= 16 and 2 | Hkv, tuning decode_kernel 2 / PATTN_DECODE_WIDE=0 keeps K2).
   if (pl->use_k2 && pl->tuning.decode_kernel != 2) pl->decode_hb = wide_decode_heads(p->num_kv_heads, G);
   // Decode segment policy (parallel tiled softmax): target work items per SM and the
   // shortest segment.  The tuning leaf's values apply to the kernel it was measured with (its

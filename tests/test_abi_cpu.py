@@ -95,7 +95,7 @@ def test_workspace_and_planned_launches(lib, monkeypatch):
     assert lib.planned_kernels(pb) == (1 << lib.KERNEL_METADATA) | (1 << lib.KERNEL_DECODE) | (
         1 << lib.KERNEL_REDUCE)
     monkeypatch.delenv("PATTN_DECODE_WIDE")
-    pg = _problem(lib, Hq=64, Hkv=4, D=128, dtype=1, T=64, B=64, nb=16448, maxb=257)  # G = 16: K2
+    pg = _problem(lib, Hq=128, Hkv=4, D=128, dtype=1, T=64, B=64, nb=16448, maxb=257)  # G = 32: K2
     pg.max_query_len = 1
     assert not lib.planned_kernels(pg) & lib.PLAN_DECODE_WIDE
     pb.max_query_len = 2048

@@ -641,7 +641,7 @@ def test_shape_fuzz(i):
 
 
 # ---------------------------------------------------------------- decode kernels K2 and K2W
-# K2W (head-wide TMA boxes, HB KV heads per item) is the default decode kernel when G <= 8 and
+# K2W (head-wide TMA boxes, HB KV heads per item) is the default decode kernel when G <= 16 and
 # 2 | Hkv; K2 (one KV head per item) stays for the rest and under PATTN_DECODE_WIDE=0.  Both are
 # checked against the oracle on the same batches, for every HB K2W instantiates (PATTN_DECODE_WIDE_HB
 # caps it), and the plan is checked to route where it says.
@@ -653,6 +653,9 @@ DECODE_CASES = [
     ((16, 2), 64, 48, "bf16", "NHD"),    # G = 8, D = 64, HB = 2
     ((32, 8), 64, 16, "f16", "HND"),
     ((12, 6), 128, 16, "bf16", "NHD"),   # Hkv = 6 -> HB = 2
+    ((96, 8), 128, 16, "bf16", "HND"),   # G = 12: two head groups per KV head (8 + 4)
+    ((64, 4), 64, 32, "f16", "NHD"),     # G = 16: two full head groups, D = 64
+    ((40, 2), 128, 16, "bf16", "NHD"),   # G = 20 > 16: K2 in every case
 ]
 
 
@@ -671,7 +674,7 @@ def test_decode_wide_and_narrow(case, hb_cap, monkeypatch):
     db = DeviceBatch(batch)
     prob = P.make_problem(db.q, db.k, w.num_kv_heads, w.block_size, db.bt, w.num_seqs, kv_layout=layout)
     wide = bool(P.planned_kernels(prob) & P.PLAN_DECODE_WIDE)
-    assert wide == (hb_cap > 0 and heads[0] // heads[1] <= 8), (heads, hb_cap, wide)
+    assert wide == (hb_cap > 0 and heads[0] // heads[1] <= 16), (heads, hb_cap, wide)
     ref = O.batch_attention(batch)
     for flags in (0, P.FLAG_FORCE_SPLIT, P.FLAG_NO_SPLIT):
         assert_close(out_f64(db.run(flags=flags)), ref, dt, f"{w.name} hb<={hb_cap} flags={flags}")

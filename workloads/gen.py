@@ -133,6 +133,8 @@ ATTRIBUTION: Dict[str, Workload] = {
     "x_d64_mixed": Workload("x_d64_mixed", tuple([(0, 2048)] * 8 + [(4096, 1)] * 56), 32, 8, 64, 16, "bf16"),
     # block size 7 (not a multiple of 16): long decodes split on K2W with cp.async-gathered rows, merged by K3
     "x_bs7_decode32k": Workload("x_bs7_decode32k", tuple((32768, 1) for _ in range(8)), 32, 8, 128, 7, "bf16"),
+    # GQA 12:1 decode (96 query / 8 KV heads, e.g. Mistral-Large): K2W with two head groups per KV head
+    "x_g12_decode8k": Workload("x_g12_decode8k", tuple((8192, 1) for _ in range(32)), 96, 8, 128, 16, "bf16"),
     # config 3's mix with block size 7: K1 and K2W gather K/V rows with cp.async (no TMA box fits a page)
     "x_bs7_mixed": Workload("x_bs7_mixed", tuple([(0, 2048)] * 8 + [(4096, 1)] * 56), 32, 8, 128, 7, "bf16"),
 }
