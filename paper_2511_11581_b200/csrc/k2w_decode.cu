@@ -165,19 +165,20 @@ __global__ void __launch_bounds__((HB * HGW + (kGather ? 4 : 1)) * 32, 1)
       const int32_t* bt = p.block_table + (int64_t)x.b * p.bt_stride;
       const int nsb = (x.k1 - x.k0 + kSub - 1) / kSub;
       for (int j = 0; j < nsb; ++j) {
+        // rows past the segment's keys are left unwritten: their scores are masked by select and
+        // the consumers zero those V rows
         const int key = x.k0 + j * kSub + t;
-        const uint8_t* srck = nullptr;
-        int64_t row = 0;
-        if (key < x.k1) {
+        const bool has_row = key < x.k1;
+        int64_t row = 0;  // byte offset of (page, slot, first head of the box, chunk)
+        if (has_row) {
           const int pg = key / p.bs;
           row = ((int64_t)__ldg(bt + pg) * p.kv_st_blk + (int64_t)(key - pg * p.bs) * p.kv_st_tok +
                  (int64_t)(x.hb * HB) * p.kv_st_head + ch * 8) * esz;
-          srck = static_cast<const uint8_t*>(p.k);
         }
 #pragma unroll
         for (int op = 0; op < 2; ++op) {  // K, then V
           mbar_wait(&empty[s], ph ^ 1u);
-          if (srck) {
+          if (has_row) {
             const uint8_t* src = static_cast<const uint8_t*>(op ? p.v : p.k) + row;
             const uint32_t dst = smem_u32(ring + (size_t)s * S::kOpBytes) + t * 128 + ((ch ^ (t & 7)) << 4);
 #pragma unroll
