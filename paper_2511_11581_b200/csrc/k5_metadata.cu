@@ -24,18 +24,26 @@ namespace {
 
 constexpr int kMaxThreads = 1024;
 
-// Block-wide sum of one unsigned 64-bit value per thread (all threads get the total).
-__device__ unsigned long long block_sum_u64(unsigned long long v, unsigned long long* s_red) {
+// Block-wide sums of N unsigned 64-bit values per thread at once (all threads get the totals):
+// one pair of barriers for all N (K5 is a single CTA on the critical path of every call).
+template <int N>
+__device__ void block_sum_u64(unsigned long long (&v)[N], unsigned long long (*s_red)[32]) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  if (lane == 0) s_red[warp] = v;
-  __syncthreads();
-  unsigned long long t = lane < nw ? s_red[lane] : 0ull;
+  for (int i = 0; i < N; ++i) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    for (int o = 16; o > 0; o >>= 1) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
+    if (lane == 0) s_red[i][warp] = v[i];
+  }
   __syncthreads();
-  return t;
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    unsigned long long t = lane < nw ? s_red[i][lane] : 0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    v[i] = t;
+  }
+  __syncthreads();
 }
 
 // Block-wide exclusive scan of two ints per thread at once (x: Q blocks, y: decode
@@ -76,7 +84,7 @@ __device__ int2 block_exclusive_scan2(int2 v, int2* s_warp, int2* total) {
 // (one pass over the batch when B <= blockDim: per-sequence values stay in registers).
 __global__ void __launch_bounds__(kMaxThreads) k5_metadata(Params p) {
   pdl_trigger();  // the next kernel may be scheduled now; it waits for this grid (pdl_wait)
-  __shared__ unsigned long long s_red[32];
+  __shared__ unsigned long long s_red[5][32];
   __shared__ int2 s_scan[32];
   const int B = p.B;
   const int nt = blockDim.x;
@@ -102,14 +110,10 @@ __global__ void __launch_bounds__(kMaxThreads) k5_metadata(Params p) {
         my_tiles += (unsigned long long)((ctx + min(t0 + p.block_q, qb) + 127) / 128);
     }
   }
-  const unsigned long long n_dec = block_sum_u64(my_dec, s_red);
-  const unsigned long long n_viol = block_sum_u64(my_viol, s_red);
-  const unsigned long long dec_blocks = block_sum_u64(my_blocks, s_red);
-  unsigned long long tiles = 0, keys = 0;
-  if (p.partition) {
-    tiles = block_sum_u64(my_tiles, s_red);
-    keys = block_sum_u64(my_keys, s_red);
-  }
+  unsigned long long sums[5] = {my_dec, my_viol, my_blocks, my_tiles, my_keys};
+  block_sum_u64<5>(sums, s_red);
+  const unsigned long long n_dec = sums[0], n_viol = sums[1], dec_blocks = sums[2];
+  const unsigned long long tiles = p.partition ? sums[3] : 0ull, keys = p.partition ? sums[4] : 0ull;
 
   // SM partition for concurrent K1 / K2: P minimising max(prefill time on P SMs, decode
   // time on the other SMs, capped by HBM), from per-SM rates of the two kernels.
