@@ -178,6 +178,7 @@ struct Plan {
   int decode_hb = 0;  // > 0: decodes on K2W (head-wide boxes)
   int leaf_kernel = 1;  // the decode kernel the tuning leaf's decode knobs were measured with
   int decode_ctas = 2;  // K2 CTAs per SM
+  bool use_leaf_rate = false;  // the partition model takes the leaf's / env's decode rate
   bool decode_gather = false;  // K2W with cp.async-gathered entries (block size not a multiple of 16)
   int target_items = 0, min_chunk = 1, split_mode = 0, max_chunks = 0;
   int num_sms = 148;
@@ -332,6 +333,7 @@ pattn_status_t make_plan(const pattn_problem_t* p, const void* q, const void* kc
   const int items_per_sm = use_items ? pl->tuning.items_per_sm : (pl->decode_hb ? 2 : 16);
   const int min_tok = use_min ? pl->tuning.min_chunk_tokens : (pl->decode_hb ? 128 : 256);
   pl->decode_ctas = use_ctas ? pl->tuning.decode_ctas_per_sm : 2;
+  pl->use_leaf_rate = (leaf_fits || env_set("PATTN_K2_SM_GBS")) && pl->tuning.k2_sm_mbs > 0;
   if (p->flags & PATTN_FLAG_NO_SPLIT) {
     pl->split_mode = 1;
     pl->target_items = 1;
@@ -601,9 +603,9 @@ pattn_status_t run(const pattn_problem_t* p, const void* q, const void* k_cache,
     k.partition = 1;
     k.prefill_ctas_fixed = env_int("PATTN_PREFILL_SMS", 0);
     k.k1_tile_us = env_float("PATTN_K1_TILE_US", 2.8f);
-    // per-SM decode rate of the partition model: the tree / env value, else the measured
-    // default of the decode kernel in use (K2W: PATTN_K2W_SM_GBS, K2: 61 GB/s/SM)
-    k.k2_sm_gbs = pl.tuning.k2_sm_mbs > 0 ? (float)pl.tuning.k2_sm_mbs * 1e-3f
+    // per-SM decode rate of the partition model: the tree (if measured with this decode kernel) /
+    // env value, else the measured default of the decode kernel in use (K2W: 80, K2: 61 GB/s/SM)
+    k.k2_sm_gbs = pl.use_leaf_rate ? (float)pl.tuning.k2_sm_mbs * 1e-3f
                   : pl.decode_hb          ? env_float("PATTN_K2W_SM_GBS", 80.f)
                                           : 61.f;
     k.hbm_gbs = env_float("PATTN_HBM_GBS", 6300.f);
