@@ -778,3 +778,46 @@ def test_large_batch_multi_pass_metadata():
     assert plan[8:8 + B + 1].tolist() == cu_qb_ref.tolist()
     assert plan[1] == int(dec.sum())
     _check(batch, 0, "1500 sequences")
+
+
+K2W_MATRIX = [
+    # heads (Hq, Hkv), D, bs, dtype, layout -- G = 1 .. 16, TMA and gathered entries, NHD / HND
+    ((8, 8), 128, 32, "bf16", "HND"),    # G 1, HB 8
+    ((16, 8), 64, 64, "f16", "NHD"),     # G 2
+    ((16, 4), 128, 128, "bf16", "HND"),  # G 4, HB 4, bs 128
+    ((64, 8), 128, 9, "bf16", "NHD"),    # G 8, gathered (bs 9)
+    ((48, 4), 64, 16, "bf16", "HND"),    # G 12, HB 4, two head groups
+    ((32, 2), 128, 33, "f16", "HND"),    # G 16, HB 2, gathered (bs 33)
+]
+
+
+@pytest.mark.parametrize("case", range(len(K2W_MATRIX)))
+def test_k2w_matrix(case):
+    """K2W across GQA ratios 1..16 (one or two head groups per KV head), heads per box 2/4/8,
+    TMA boxes and cp.async-gathered entries, both layouts: planned as K2W, split and unsplit
+    decodes next to a prefill, matching the oracle; needles bit-exact on the same shapes."""
+    heads, D, bs, dt, layout = K2W_MATRIX[case]
+    w = Workload(f"k2wm{case}", ((5000, 1), (130, 1), (2, 1), (0, 77), (12000, 1), (700, 1)), heads[0], heads[1], D,
+                 bs, dt)
+    batch = generate(w, seed=900 + case, dist="peaked", poison=True, layout=layout)
+    db = DeviceBatch(batch)
+    p = P.make_problem(db.q, db.k, w.num_kv_heads, w.block_size, db.bt, w.num_seqs, None, layout, 77, 12001)
+    assert P.planned_kernels(p) & P.PLAN_DECODE_WIDE
+    ref = O.batch_attention(batch)
+    for flags in (0, P.FLAG_FORCE_SPLIT):
+        assert_close(out_f64(db.run(flags=flags)), ref, dt, f"{w.name} flags={flags}")
+    if dt == "bf16":
+        wn = Workload(f"k2wn{case}", ((3000, 1), (411, 1)), heads[0], heads[1], D, bs, dt)
+        nb = generate(wn, seed=950 + case, dist="needle", layout=layout)
+        out = DeviceBatch(nb).run(flags=P.FLAG_FORCE_SPLIT).cpu()
+        v = O.widen(nb.v_cache)
+        G = heads[0] // heads[1]
+        for b in range(wn.num_seqs):
+            s = int(nb.cu_seqlens_q[b])
+            for g in range(wn.num_kv_heads):
+                t = int(nb.needle_pos[b, g])
+                blk, slot = int(nb.block_table[b, t // bs]), t % bs
+                row = v[blk, g, slot] if layout == "HND" else v[blk, slot, g]
+                row = torch.from_numpy(row).to(torch.bfloat16)
+                for h in range(g * G, (g + 1) * G):
+                    assert torch.equal(out[s, h], row), (case, b, g, h, t)
