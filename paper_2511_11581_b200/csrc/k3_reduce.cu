@@ -42,10 +42,12 @@ __global__ void __launch_bounds__(256) k3_reduce(Params p) {
     if (item < n_items) {
       b = item / p.Hq;
       h = item - b * p.Hq;
-      const int qb = p.cu_seqlens_q[b + 1] - p.cu_seqlens_q[b];
-      if (p.decode_split && qb == 1) {
-        c0 = p.cu_ch[b];
-        n = p.cu_ch[b + 1] - c0;
+      // the four metadata words in one round of loads (cu_ch counts 0 segments for non-decodes)
+      const int q0 = p.cu_seqlens_q[b], q1 = p.cu_seqlens_q[b + 1];
+      const int ch0 = p.cu_ch[b], ch1 = p.cu_ch[b + 1];
+      if (p.decode_split && q1 - q0 == 1) {
+        c0 = ch0;
+        n = ch1 - ch0;
       }
     }
     const bool work = n > 1;  // n <= 1: the decode kernel wrote the final output itself
