@@ -325,17 +325,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (x.ntiles < 0) break;
         const uint8_t* gbase = static_cast<const uint8_t*>(kv ? p.v : p.k) + (int64_t)x.kvh * p.kv_st_head * esz;
         const int32_t* bt = p.block_table + (int64_t)x.b * p.bt_stride;
+        // the block-table entry of this thread's row, one tile ahead (its load latency overlaps
+        // the current tile's copies)
+        int id_next = t < x.kv_end ? __ldg(bt + t / p.bs) : 0;
         for (int jt = 0; jt < x.ntiles; ++jt) {
           const uint32_t s = cnt % nst, ph = (cnt / nst) & 1u;
           uint64_t* fullb = kv ? &bar.v_full[s] : &bar.k_full[s];
           uint64_t* emptyb = kv ? &bar.v_empty[s] : &bar.k_empty[s];
           const uint32_t dst = smem_u32(smem + (kv ? kOffV : kOffK) + s * kTile) + (t >> 3) * kGroup + (t & 7) * 128;
           const int key = jt * kN + t;
+          const int id = id_next;
+          id_next = (jt + 1 < x.ntiles && key + kN < x.kv_end) ? __ldg(bt + (key + kN) / p.bs) : 0;
           const uint8_t* src = gbase;
           int bytes = 0;  // 0: zero-fill (keys past the visible range, and past the sequence end)
           if (key < x.kv_end) {
-            const int pg = key / p.bs;
-            src = gbase + ((int64_t)__ldg(bt + pg) * p.kv_st_blk + (int64_t)(key - pg * p.bs) * p.kv_st_tok) * esz;
+            src = gbase + ((int64_t)id * p.kv_st_blk + (int64_t)(key % p.bs) * p.kv_st_tok) * esz;
             bytes = 16;
           }
           if (lane == 0) mbar_wait(emptyb, ph ^ 1u);
