@@ -235,7 +235,7 @@ typedef struct pattn_tuning {
   int32_t decode_ctas_per_sm; /* decode: resident K2 CTAs per SM, 1..4 (default 2; K2W runs one) */
   int32_t k2_sm_mbs;          /* mixed batches, two streams: decode streaming rate per SM (MB/s) that K5's
                                  SM-partition model assumes -- higher leaves more SMs to the prefill kernel
-                                 (default: the measured rate of the decode kernel in use, K2W 80000, K2 61000) */
+                                 (default: the measured rate of the decode kernel in use, K2W 100000, K2 61000) */
   int32_t serial;             /* mixed batches: 1 = prefill and decode kernels back to back on one stream
                                  even when a second stream is given; 0 = concurrent (default) */
   int32_t decode_kernel;      /* decode kernel: 1 = K2W (head-wide TMA boxes) where it applies (G <= 16,

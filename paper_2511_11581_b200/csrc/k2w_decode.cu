@@ -84,7 +84,7 @@ __device__ __forceinline__ WItem wide_item(const Params& p, int it, int ngroups)
 // HGW: head groups of <= 8 query heads per KV head (G <= 8: 1; 8 < G <= 16: 2); the consumer
 // warps are (KV head, head group) pairs.
 template <int D, int HB, typename E, bool kGather, int HGW>
-__global__ void __launch_bounds__((HB * HGW + (kGather ? 4 : 1)) * 32, 1)
+__global__ void __launch_bounds__((HB * HGW + (kGather ? 4 : 2)) * 32, 1)
     k2w_decode(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, Params p,
                int nent) {
   using S = WideShape<D, HB>;
@@ -99,7 +99,7 @@ __global__ void __launch_bounds__((HB * HGW + (kGather ? 4 : 1)) * 32, 1)
   uint64_t* item_empty = item_full + kItemRing;
   volatile int* item_ring = reinterpret_cast<volatile int*>(item_empty + kItemRing);
 
-  constexpr int kProd = kGather ? 4 : 1;  // producer warps
+  constexpr int kProd = kGather ? 4 : 2;  // producer warps (TMA: one for K boxes, one for V boxes)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   pdl_wait();  // K5's metadata (or, serial, the previous kernel's work) is complete and visible
   if (p.partition) {
@@ -195,28 +195,38 @@ __global__ void __launch_bounds__((HB * HGW + (kGather ? 4 : 1)) * 32, 1)
     }
     return;
   }
-  if (!kGather && warp == 0) {
-    // ------------------------------------------------------------ producer
-    if (lane == 0) {
-      tma_prefetch_desc(&tmK);
-      tma_prefetch_desc(&tmV);
-    }
+  if (!kGather && warp < kProd) {
+    // ------------------------------------------------------------ producers
+    // warp 0 issues the K boxes (even ring positions), warp 1 the V boxes (odd positions): two
+    // issuing threads halve the queueing of the per-request TMA issue cost.  Warp 0 claims the
+    // items; warp 1 reads them from the item ring like the consumers.
+    const int op = warp;  // 0: K, 1: V
+    const CUtensorMap* tm = op ? &tmV : &tmK;
+    if (lane == 0) tma_prefetch_desc(tm);
     const uint64_t policy = l2_policy_evict_first();  // K/V are streamed exactly once
-    // ring position of the next entry, kept incrementally (nent is a runtime value: g % nent
-    // and g / nent cost an integer division per entry on the consumers' critical path)
-    uint32_t s = 0, ph = 0;
+    // ring position of this producer's next entry, kept incrementally (nent is a runtime value:
+    // g % nent and g / nent would cost an integer division per entry); K(j) at position 2g, V(j)
+    // at 2g + 1 of the CTA's sub-block sequence
+    uint32_t s = (uint32_t)op % (uint32_t)nent, ph = 0;
     for (uint32_t ni = 0;; ++ni) {
       int it = 0;
-      if (lane == 0) {
-        const uint32_t slot = ni % kItemRing;
-        mbar_wait(&item_empty[slot], ((ni / kItemRing) & 1u) ^ 1u);
-        it = atomicAdd(p.hdr + kHdrDecodeCounter, 1);
-        item_ring[slot] = it;
-        mbar_arrive(&item_full[slot]);
+      const uint32_t slot = ni % kItemRing;
+      if (op == 0) {
+        if (lane == 0) {
+          mbar_wait(&item_empty[slot], ((ni / kItemRing) & 1u) ^ 1u);
+          it = atomicAdd(p.hdr + kHdrDecodeCounter, 1);
+          item_ring[slot] = it;
+          mbar_arrive(&item_full[slot]);
+        }
+        it = __shfl_sync(0xffffffffu, it, 0);
+      } else {
+        mbar_wait(&item_full[slot], (ni / kItemRing) & 1u);
+        it = item_ring[slot];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&item_empty[slot]);
       }
-      it = __shfl_sync(0xffffffffu, it, 0);
       if (it >= n_items) {
-        if (lane == 0) pdl_trigger();  // no more items here: K3 may be scheduled
+        if (op == 0 && lane == 0) pdl_trigger();  // no more items here: K3 may be scheduled
         break;
       }
       const WItem x = wide_item(p, it, ngroups);
@@ -228,15 +238,12 @@ __global__ void __launch_bounds__((HB * HGW + (kGather ? 4 : 1)) * 32, 1)
           const int blk = __shfl_sync(0xffffffffu, id, jj);
           if (lane == 0) {
             const int slot0 = ((j0 + jj) % n16) * kSub;
-#pragma unroll
-            for (int op = 0; op < 2; ++op) {  // K, then V
-              mbar_wait(&empty[s], ph ^ 1u);
-              mbar_arrive_expect_tx(&full[s], S::kOpBytes);
-              tma_load_5d_hint(ring + (size_t)s * S::kOpBytes, op ? &tmV : &tmK, &full[s], 0, slot0, 0, x.hb * HB,
-                               blk, policy);
-              if (++s == (uint32_t)nent) s = 0, ph ^= 1u;
-            }
+            mbar_wait(&empty[s], ph ^ 1u);
+            mbar_arrive_expect_tx(&full[s], S::kOpBytes);
+            tma_load_5d_hint(ring + (size_t)s * S::kOpBytes, tm, &full[s], 0, slot0, 0, x.hb * HB, blk, policy);
           }
+          s += 2;  // this producer's next position (positions alternate K, V)
+          if (s >= (uint32_t)nent) s -= (uint32_t)nent, ph ^= 1u;
         }
       }
     }
@@ -433,7 +440,7 @@ cudaError_t launch_wg(const Params& p, const DecodeLaunch& dl, const CUtensorMap
   auto kern = k2w_decode<D, HB, E, G, HGW>;
   cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(kern), dl.smem);
   if (e != cudaSuccess) return e;
-  return launch_pdl(kern, dim3(dl.grid), dim3((HB * HGW + (G ? 4 : 1)) * 32), dl.smem, stream, tmK, tmV, p,
+  return launch_pdl(kern, dim3(dl.grid), dim3((HB * HGW + (G ? 4 : 2)) * 32), dl.smem, stream, tmK, tmV, p,
                     dl.stages);
 }
 template <int D, int HB, typename E>

@@ -604,9 +604,10 @@ pattn_status_t run(const pattn_problem_t* p, const void* q, const void* k_cache,
     k.prefill_ctas_fixed = env_int("PATTN_PREFILL_SMS", 0);
     k.k1_tile_us = env_float("PATTN_K1_TILE_US", 2.8f);
     // per-SM decode rate of the partition model: the tree (if measured with this decode kernel) /
-    // env value, else the measured default of the decode kernel in use (K2W: 80, K2: 61 GB/s/SM)
+    // env value, else the measured default of the decode kernel in use (K2W: 100, K2: 61 GB/s/SM;
+    // K2W swept 80 / 90 / 100 on configs 3 and 5: 362.5 / 359.5 / 358.1 us and 2653 / 2635 / 2643 us)
     k.k2_sm_gbs = pl.use_leaf_rate ? (float)pl.tuning.k2_sm_mbs * 1e-3f
-                  : pl.decode_hb          ? env_float("PATTN_K2W_SM_GBS", 80.f)
+                  : pl.decode_hb          ? env_float("PATTN_K2W_SM_GBS", 100.f)
                                           : 61.f;
     k.hbm_gbs = env_float("PATTN_HBM_GBS", 6300.f);
   }

@@ -38,7 +38,7 @@ KNOBS = ["items_per_sm", "min_chunk_tokens", "decode_ctas_per_sm", "k2_sm_mbs", 
 # libpattn's built-in value of each knob (used where a tree leaf or record holds 0)
 # 0 where the default depends on the decode kernel the planner picks: items_per_sm (K2 16, K2W 2),
 # min_chunk_tokens (K2 256, K2W 128),
-# k2_sm_mbs (the kernel's measured per-SM rate: K2W 80 GB/s, K2 61 GB/s)
+# k2_sm_mbs (the kernel's measured per-SM rate: K2W 100 GB/s, K2 61 GB/s)
 DEFAULTS = {"items_per_sm": 0, "min_chunk_tokens": 0, "decode_ctas_per_sm": 2, "k2_sm_mbs": 0, "serial": 0,
             "decode_kernel": 1}
 
