@@ -249,7 +249,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #ifdef PATTN_PARTITION_BLOCKIDX  // A/B: the round-1 rule (CTA index, launch-order dependent)
   if (p.partition && (int)blockIdx.x >= p.hdr[kHdrPrefillCtas]) return;
 #else
-  if (p.partition && blockIdx.x != 0 && !partition_prefill_sm(sm_id(), p.hdr[kHdrPrefillCtas], p.num_sms)) return;
+  // A CTA that reaches a decode SM only after the decode kernel's queue is empty (a replayed graph
+  // may start the decode branch first: K1's CTAs for those SMs then wait behind the decode CTAs)
+  // stays and takes prefill items -- K1 then spreads onto the SMs the decode side has finished.
+  if (p.partition && blockIdx.x != 0 && !partition_prefill_sm(sm_id(), p.hdr[kHdrPrefillCtas], p.num_sms) &&
+      *reinterpret_cast<volatile int*>(p.hdr + kHdrDecodeClaimed) == 0)
+    return;
 #endif
 #ifdef PATTN_TRACE
   const int trace_role = warp == 15 ? -1 : warp == 1 ? 0 : warp == 0 ? 3 : warp == 3 ? 4 : warp == 4 ? 1 : 2;

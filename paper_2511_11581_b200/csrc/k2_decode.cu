@@ -169,7 +169,10 @@ __global__ void __launch_bounds__((NCW + kNP) * 32, 1)
       }
       it = __shfl_sync(0xffffffffu, it, 0);
       if (it >= n_items) {
-        if (pw == 0 && lane == 0) pdl_trigger();  // no more items here: K3 may be scheduled
+        if (pw == 0 && lane == 0) {
+          pdl_trigger();                              // no more items here: K3 may be scheduled
+          atomicExch(p.hdr + kHdrDecodeClaimed, 1);  // and K1's late CTAs may take decode SMs
+        }
         break;
       }
       const Item x = decode_item(p, it);

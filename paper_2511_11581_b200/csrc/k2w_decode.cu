@@ -158,7 +158,10 @@ __global__ void __launch_bounds__((HB * HGW + (kGather ? 4 : 2)) * 32, 1)
         if (lane == 0) mbar_arrive(&item_empty[slot]);
       }
       if (it >= n_items) {
-        if (warp == 0 && lane == 0) pdl_trigger();
+        if (warp == 0 && lane == 0) {
+          pdl_trigger();
+          atomicExch(p.hdr + kHdrDecodeClaimed, 1);  // (K1's late CTAs may take decode SMs now)
+        }
         break;
       }
       const WItem x = wide_item(p, it, ngroups);
@@ -226,7 +229,10 @@ __global__ void __launch_bounds__((HB * HGW + (kGather ? 4 : 2)) * 32, 1)
         if (lane == 0) mbar_arrive(&item_empty[slot]);
       }
       if (it >= n_items) {
-        if (op == 0 && lane == 0) pdl_trigger();  // no more items here: K3 may be scheduled
+        if (op == 0 && lane == 0) {
+          pdl_trigger();                              // no more items here: K3 may be scheduled
+          atomicExch(p.hdr + kHdrDecodeClaimed, 1);  // and K1's late CTAs may take decode SMs
+        }
         break;
       }
       const WItem x = wide_item(p, it, ngroups);

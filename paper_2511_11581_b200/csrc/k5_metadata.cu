@@ -186,6 +186,7 @@ __global__ void __launch_bounds__(kMaxThreads) k5_metadata(Params p) {
     p.hdr[kHdrPrefillCounter] = 0;
     p.hdr[kHdrDecodeCounter] = 0;
     p.hdr[kHdrHintViolation] = n_viol ? 1 : 0;
+    p.hdr[kHdrDecodeClaimed] = 0;
     p.hdr[kHdrPrefillCtas] = P;
   }
 }

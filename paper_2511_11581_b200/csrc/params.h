@@ -17,6 +17,8 @@ enum HdrWord {
   kHdrDecodeCounter = 6,
   kHdrPrefillCtas = 7,   // two-stream SM partition: K1 CTAs that work (the rest exit at once)
   kHdrHintViolation = 8, // K5: 1 if some q_b exceeds the max_query_len hint (the plan may miss it)
+  kHdrDecodeClaimed = 9, // 1 once the decode kernel's item queue is empty (two-stream partition: K1
+                         // CTAs that find their SM only after that may work on prefill items)
   kHdrWords = 64
 };
 
