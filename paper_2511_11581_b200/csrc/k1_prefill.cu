@@ -4,33 +4,32 @@
 // BLOCK_Q consecutive query tokens x the G query heads that share one KV head into a
 // BLOCK_M-row tile (token-major / head-minor, reading R8), so every K/V tile is loaded once
 // per Q block and shared by all rows.  Here BLOCK_M = 256 = two 128-row halves (a, b), each
-// its own UMMA M=128 accumulator, so BLOCK_Q = 256/G.  KV tiles of 128 keys = 8 sub-blocks
-// of 16 keys gathered through the block table from any block size that is a multiple of 16
-// (tile size decoupled from BLOCK_SIZE, §4.6).  The tiled (online) softmax of
-// §4.1 runs between the two contractions.
+// its own UMMA M=128 accumulator, so BLOCK_Q = 2 * floor(128/G) (padding rows when G does not
+// divide 128).  KV tiles of 64 keys = 4 sub-blocks of 16 keys gathered through the block
+// table -- one TMA box per sub-block from any block size that is a multiple of 16, or, for
+// other block sizes, row by row with cp.async (kGather) -- tile size decoupled from
+// BLOCK_SIZE (§4.6).  The tiled (online) softmax of §4.1 runs between
+// the two contractions.
 //
 // One CTA per SM, persistent over (Q block, KV head) work items (static launch grid,
-// P:401-406), longest (last) Q blocks first.  Items are claimed dynamically: warp 0 takes
-// the next item index from a global atomic counter (reset by K5) and publishes it to the
-// CTA's other role warps through an 8-deep shared-memory ring, so a CTA that shares its SM
-// with the decode kernel (two streams) or drew short items simply claims fewer items.  Warp roles (384 threads):
-//   warp 0       TMA producer: Q (both halves, 4 boxes) and the K / V tiles (2 boxes per
-//                16-key sub-block; sub-blocks past the visible range are requested at block
-//                index num_blocks, out of bounds, so TMA zero-fills them) into K and V rings.
-//   warp 1       MMA issuer (one thread), per KV tile j:
-//                  PV_a(j-1)  O_a += P_a V   (P_a bf16 in TMEM, aliased on S_a; V MN-major smem)
-//                  S_a(j)     S_a  = Q_a K^T (Q, K K-major SW128 smem)
-//                  PV_b(j-1), S_b(j)
-//                so the two softmax warpgroups ping-pong: while one works on its S tile the
-//                tensor pipe runs the other half's PV and S.  tcgen05.commit -> mbarriers.
-//   warp 2       TMEM allocator: 512 columns = S_a | S_b | O_a | O_b (128 each).
-//   warps 4..7   softmax WG a (thread r owns row r of half a = TMEM lane r)
-//   warps 8..11  softmax WG b: tcgen05.ld of the S row, causal mask (row limit ctx+i+1,
-//                P:316-317), max, exp2, row sum; lazy rescale of O in TMEM only when the
-//                running max grows by > 2^8 (exact: p <= 256 otherwise); P (bf16) written
-//                back into TMEM over S with tcgen05.st; epilogue O / l -> bf16 -> out.
-// V rows past the sequence end inside the last sub-block may hold NaN (reading R13): WG a
-// zeroes them in shared memory before PV_a (PV_b is issued after PV_a).
+// P:401-406), longest (last) Q blocks first, claimed dynamically from a global counter (reset
+// by K5) by a scheduler warp that publishes them to the other roles through a shared-memory
+// ring, so a CTA that shares the GPU with the decode kernel (two streams) or drew short items
+// simply claims fewer.  Warp roles (16 warps, setmaxnreg-rebalanced registers):
+//   warps 0, 2 / 3, 12  TMA producers of the K / V rings (two sub-blocks each per tile;
+//                sub-blocks past the visible range are requested out of bounds: zero fill)
+//   warp 14      Q producer (both halves), warp 13 item scheduler, warp 2 also allocates TMEM
+//   warps 1, 15  MMA issuers for half a / b (one elected lane): S_h(j) = Q_h K^T into S buffer
+//                j & 1 (SS mode), then PV_h(j-1): O_h += P_h V with P (bf16) in TMEM aliased on
+//                its S buffer (TS mode) -- the softmax of tile j overlaps PV(j-1).
+//   TMEM (512 columns): S_a0 | S_a1 | S_b0 | S_b1 (64 each) | O_a | O_b (128 each, D = 128)
+//   warps 4..7 / 8..11  softmax warpgroups of half a / b (thread r owns row r = TMEM lane r):
+//                tcgen05.ld of the S row, causal mask on diagonal / tail tiles (row limit
+//                ctx+i+1), max, exp2, row sum; lazy rescale of O in TMEM only when
+//                the running max grows by > 2^8 (exact: p <= 256 otherwise); P written back into
+//                TMEM with tcgen05.st; epilogue O / l -> bf16 -> 128B-swizzled staging -> TMA store.
+// V rows past the sequence end inside the last sub-block may hold NaN (reading R13): the
+// softmax warpgroups zero them in shared memory before releasing P.
 #include "common.cuh"
 #include "kernels.h"
 
