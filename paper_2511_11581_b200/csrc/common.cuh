@@ -196,17 +196,10 @@ PATTN_DEVICE int sm_id() {
 
 // Two-stream SM partition: does SM `smid` belong to the prefill kernel when it owns P of the N
 // SMs?  The P lowest SM IDs.  Measured against spreading the P SMs evenly over the ID range
-// (a Bresenham selection, -DPATTN_PARTITION_SPREAD): contiguous IDs are 0.9 % faster on config
-// 3 eager (385.4 vs 388.8 us) and 1.5 % under graph replay -- K1's K/V tiles are shared by the
-// Q blocks of a sequence, and keeping K1's SMs together keeps those re-reads closer in L2.
-PATTN_DEVICE bool partition_prefill_sm(int smid, int P, int N) {
-  if (smid >= N) return false;
-#ifdef PATTN_PARTITION_SPREAD
-  return ((smid + 1) * P) / N > (smid * P) / N;
-#else
-  return smid < P;
-#endif
-}
+// (a Bresenham selection, round 2): contiguous IDs are 0.9 % faster on config 3 eager (385.4 vs
+// 388.8 us) and 1.5 % under graph replay -- K1's K/V tiles are shared by the Q blocks of a
+// sequence, and keeping K1's SMs together keeps those re-reads closer in L2.
+PATTN_DEVICE bool partition_prefill_sm(int smid, int P, int N) { return smid < N && smid < P; }
 
 // Programmatic dependent launch (PDL).  A kernel launched with programmatic stream
 // serialization may start while its predecessor in the stream still runs; pdl_wait() blocks

@@ -241,20 +241,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   PATTN_CTA_BEGIN(k1);
   pdl_wait();  // K5's metadata (and the SM partition) is complete and visible
-  // two-stream SM partition (K5's choice): K1 works on P SMs spread over the %smid range; a CTA
-  // placed on another SM leaves it to the decode kernel at once.  Keyed on the physical SM (not blockIdx),
-  // so it holds whichever kernel the hardware (or a replayed CUDA graph, whose two branches
-  // start in either order) launches first.  CTA 0 always works (progress guarantee).
-#ifdef PATTN_PARTITION_BLOCKIDX  // A/B: the round-1 rule (CTA index, launch-order dependent)
-  if (p.partition && (int)blockIdx.x >= p.hdr[kHdrPrefillCtas]) return;
-#else
-  // A CTA that reaches a decode SM only after the decode kernel's queue is empty (a replayed graph
+  // two-stream SM partition (K5's choice): K1 works on the P lowest SM IDs; a CTA placed on
+  // another SM leaves it to the decode kernel at once.  Keyed on the physical SM (not blockIdx:
+  // the round-1 rule, launch-order dependent), so it holds whichever kernel the hardware (or a
+  // replayed CUDA graph, whose two branches start in either order) launches first.  CTA 0
+  // always works (progress guarantee).  A CTA that reaches a decode SM only after the decode kernel's queue is empty (a replayed graph
   // may start the decode branch first: K1's CTAs for those SMs then wait behind the decode CTAs)
   // stays and takes prefill items -- K1 then spreads onto the SMs the decode side has finished.
   if (p.partition && blockIdx.x != 0 && !partition_prefill_sm(sm_id(), p.hdr[kHdrPrefillCtas], p.num_sms) &&
       *reinterpret_cast<volatile int*>(p.hdr + kHdrDecodeClaimed) == 0)
     return;
-#endif
 #ifdef PATTN_TRACE
   const int trace_role = warp == 15 ? -1 : warp == 1 ? 0 : warp == 0 ? 3 : warp == 3 ? 4 : warp == 4 ? 1 : 2;
   unsigned int trace_cnt = 0;

@@ -41,11 +41,6 @@ namespace pattn {
 namespace {
 
 constexpr int kSub = 16;  // keys per ring stage (one mma M tile)
-#ifdef PATTN_PARTITION_BLOCKIDX
-#define PATTN_PARTITION_BLOCKIDX_ON 1
-#else
-#define PATTN_PARTITION_BLOCKIDX_ON 0
-#endif
 constexpr int kItemRing = 16;
 #ifndef PATTN_K2_NP
 #define PATTN_K2_NP 4  // measured: per-SM decode rate +8% on 36 SMs vs 2 producers
@@ -111,7 +106,7 @@ __global__ void __launch_bounds__((NCW + kNP) * 32, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   PATTN_CTA_BEGIN(k2);
   pdl_wait();  // K5's metadata (or, serial, the previous kernel's work) is complete and visible
-  if (p.partition && !PATTN_PARTITION_BLOCKIDX_ON) {
+  if (p.partition) {
     // two-stream SM partition: K5's P SMs belong to the prefill kernel K1 while it
     // still has Q blocks to claim -- a decode CTA placed there first (graph replays launch the
     // two branches in either order) leaves at once.  CTA 0 always works (progress guarantee).
