@@ -45,7 +45,9 @@
  *     PATTN_MIN_CHUNK_TOKENS, PATTN_DECODE_CTAS, PATTN_K2_SM_GBS, PATTN_SERIAL,
  *     PATTN_DECODE_WIDE (1 / 0 = decode_kernel 1 / 2) (see pattn_tuning_t),
  *     PATTN_PREFILL_SMS (fixed two-stream split), PATTN_DISABLE_K1, PATTN_DECODE_WIDE_HB
- *     (cap on K2W's heads per box).
+ *     (cap on K2W's heads per box), PATTN_K2W_SM_GBS (the partition model's K2W rate),
+ *     PATTN_DECODE_SMS / PATTN_DECODE_RING_KB (decode grid and ring size, for sweeps),
+ *     PATTN_TARGET_ITEMS / PATTN_MIN_CHUNK_BLOCKS (segment plan), PATTN_NO_PDL.
  */
 #ifndef PATTN_H_
 #define PATTN_H_
