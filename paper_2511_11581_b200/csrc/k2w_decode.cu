@@ -32,6 +32,9 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "trace.cuh"
+
+PATTN_CTA_TRACE_DEFINE(k2w)
 
 namespace pattn {
 namespace {
@@ -101,6 +104,7 @@ __global__ void __launch_bounds__((HB * HGW + (kGather ? 4 : 2)) * 32, 1)
 
   constexpr int kProd = kGather ? 4 : 2;  // producer warps (TMA: one for K boxes, one for V boxes)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  PATTN_CTA_BEGIN(k2w);
   pdl_wait();  // K5's metadata (or, serial, the previous kernel's work) is complete and visible
   if (p.partition) {
     // two-stream SM partition (as K2): K5's P SMs belong to the prefill kernel while it still
@@ -266,7 +270,8 @@ __global__ void __launch_bounds__((HB * HGW + (kGather ? 4 : 2)) * 32, 1)
   const uint32_t ring_u32 = smem_u32(ring);
   const int G = p.G;
   uint32_t s = 0, ph = 0;  // ring position of the next stage (incremental, as the producer)
-  for (uint32_t ni = 0;; ++ni) {
+  uint32_t ni = 0;  // items consumed (the trace build records it per CTA)
+  for (;; ++ni) {
     const uint32_t slot = ni % kItemRing;
     mbar_wait(&item_full[slot], (ni / kItemRing) & 1u);
     const int it = item_ring[slot];
@@ -438,6 +443,7 @@ __global__ void __launch_bounds__((HB * HGW + (kGather ? 4 : 2)) * 32, 1)
       }
     }
   }
+  if (warp == kProd && lane == 0) PATTN_CTA_END(k2w, ni);
 }
 
 template <int D, int HB, typename E, bool G, int HGW>
