@@ -47,7 +47,9 @@
  *     PATTN_PREFILL_SMS (fixed two-stream split), PATTN_DISABLE_K1, PATTN_DECODE_WIDE_HB
  *     (cap on K2W's heads per box), PATTN_K2W_SM_GBS (the partition model's K2W rate),
  *     PATTN_DECODE_SMS / PATTN_DECODE_RING_KB (decode grid and ring size, for sweeps),
- *     PATTN_TARGET_ITEMS / PATTN_MIN_CHUNK_BLOCKS (segment plan), PATTN_NO_PDL.
+ *     PATTN_TARGET_ITEMS / PATTN_MIN_CHUNK_BLOCKS (segment plan), PATTN_NO_PDL,
+ *     PATTN_K1_TILE_US (the partition model's K1 cost per tile), PATTN_K1_GROUP_MB (K1's
+ *     claim groups for batches of equal Q-block counts; results do not depend on it).
  */
 #ifndef PATTN_H_
 #define PATTN_H_

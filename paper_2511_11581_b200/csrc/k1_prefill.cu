@@ -170,9 +170,22 @@ struct ItemSlot {
 constexpr uint32_t kOffItems = sizeof(Bars);
 static_assert(sizeof(Bars) + kItemRing * sizeof(ItemSlot) <= kBarBlock, "barrier block");
 
-__device__ __forceinline__ Item prefill_item(const Params& p, int total_qb, int it, int lane) {
+__device__ __forceinline__ Item prefill_item(const Params& p, int total_qb, int qb_uniform, int qb_group, int it,
+                                             int lane) {
   Item x;
-  const int j = total_qb - 1 - it / p.Hkv;  // last Q blocks (longest key range) first
+  // Claim order, longest key range first: the Q blocks of a sequence from its last one; when all
+  // Q-block sequences have the same number u of Q blocks (K5), rank by rank across a group of
+  // g sequences (the last Q block of each, then each second-to-last, ...; groups in order, g
+  // from an L2 budget) -- the per-sequence order alone leaves a late sequence's longest items
+  // for the end of the queue (config 3 measured a 57 us spread of K1's CTA end times).
+  const int q = it / p.Hkv;
+  int j = total_qb - 1 - q;
+  if (qb_uniform > 0) {
+    const int u = qb_uniform, m = total_qb / u, gu = qb_group * u;
+    const int gi = q / gu, qq = q - gi * gu, gs = min(qb_group, m - gi * qb_group);
+    const int r = qq / gs, i = qq - r * gs;
+    j = (gi * qb_group + i) * u + (u - 1 - r);
+  }
   x.kvh = it % p.Hkv;
   x.b = upper_bound_minus1_warp(p.cu_qb, p.B, j, lane);  // App. B P:46 (warp-cooperative search)
   const int qblk = j - __ldg(p.cu_qb + x.b);
@@ -287,6 +300,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = bar.tmem_base;
 
   const int total_qb = p.hdr[kHdrTotalQBlocks];
+  const int qb_uniform = p.hdr[kHdrQbUniform], qb_group = p.hdr[kHdrQbGroup];
   const int n_items = total_qb * p.Hkv;
   const int G = p.G;
   const int bq_half = p.block_q / 2;  // tokens per 128-row half
@@ -489,7 +503,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         it = __shfl_sync(0xffffffffu, it, 0);
         volatile ItemSlot* e = ring + slot;
         if (it < n_items) {
-          const Item x = prefill_item(p, total_qb, it, lane);
+          const Item x = prefill_item(p, total_qb, qb_uniform, qb_group, it, lane);
           const int nsb_valid = (x.kv_end + 15) / 16;
           // (gathered producers look their rows up themselves: no prefetch, and n16 = 0 there)
           const int id = (!kGather && lane < 8 && lane < nsb_valid)

@@ -84,7 +84,7 @@ __device__ int2 block_exclusive_scan2(int2 v, int2* s_warp, int2* total) {
 // (one pass over the batch when B <= blockDim: per-sequence values stay in registers).
 __global__ void __launch_bounds__(kMaxThreads) k5_metadata(Params p) {
   pdl_trigger();  // the next kernel may be scheduled now; it waits for this grid (pdl_wait)
-  __shared__ unsigned long long s_red[5][32];
+  __shared__ unsigned long long s_red[9][32];
   __shared__ int2 s_scan[32];
   const int B = p.B;
   const int nt = blockDim.x;
@@ -94,6 +94,8 @@ __global__ void __launch_bounds__(kMaxThreads) k5_metadata(Params p) {
   // K1 (Q block, 128-key tile) pairs and decode keys)
   int q0 = 0, L0 = 0;  // this thread's sequence when one_pass
   unsigned long long my_blocks = 0, my_tiles = 0, my_keys = 0, my_dec = 0, my_viol = 0;
+  // Q-block sequences: count, sum of their Q blocks, of squares, of their keys
+  unsigned long long my_qs = 0, my_nqb = 0, my_nqb2 = 0, my_qkeys = 0;
   for (int b = threadIdx.x; b < B; b += nt) {
     const int qb = __ldg(p.cu_seqlens_q + b + 1) - __ldg(p.cu_seqlens_q + b);
     const int L = __ldg(p.seq_lens + b);
@@ -104,16 +106,36 @@ __global__ void __launch_bounds__(kMaxThreads) k5_metadata(Params p) {
       my_dec += 1;
       my_blocks += (unsigned long long)((L + p.bs - 1) / p.bs);
       my_keys += (unsigned long long)L;
-    } else if (p.partition && qb > 0) {
-      const int ctx = L - qb;
-      for (int t0 = 0; t0 < qb; t0 += p.block_q)
-        my_tiles += (unsigned long long)((ctx + min(t0 + p.block_q, qb) + 127) / 128);
+    } else if (qb > 0) {
+      const unsigned long long nqb = (unsigned long long)((qb + p.block_q - 1) / p.block_q);
+      my_qs += 1;
+      my_nqb += nqb;
+      my_nqb2 += nqb * nqb;
+      my_qkeys += (unsigned long long)L;
+      if (p.partition) {
+        const int ctx = L - qb;
+        for (int t0 = 0; t0 < qb; t0 += p.block_q)
+          my_tiles += (unsigned long long)((ctx + min(t0 + p.block_q, qb) + 127) / 128);
+      }
     }
   }
-  unsigned long long sums[5] = {my_dec, my_viol, my_blocks, my_tiles, my_keys};
-  block_sum_u64<5>(sums, s_red);
+  unsigned long long sums[9] = {my_dec, my_viol, my_blocks, my_tiles, my_keys, my_qs, my_nqb, my_nqb2, my_qkeys};
+  block_sum_u64<9>(sums, s_red);
   const unsigned long long n_dec = sums[0], n_viol = sums[1], dec_blocks = sums[2];
   const unsigned long long tiles = p.partition ? sums[3] : 0ull, keys = p.partition ? sums[4] : 0ull;
+  // Every Q-block sequence has the same number of Q blocks (sum of squares x count == square of
+  // the sum) -> K1 claims its items rank by rank across a group of sequences (the r-th last Q
+  // block of each before any (r+1)-th last): longest first within the group.  Groups hold as
+  // many sequences as fit k1_group_mb of K/V (L2 reuse: all Q blocks of a sequence read its K/V).
+  const unsigned long long n_qs = sums[5], s_nqb = sums[6], s_nqb2 = sums[7], s_qkeys = sums[8];
+  const int qb_uniform = (n_qs > 0 && s_nqb2 * n_qs == s_nqb * s_nqb) ? (int)(s_nqb / n_qs) : 0;
+  int qb_group = 1;
+  if (qb_uniform > 0) {
+    const double seq_bytes = (double)s_qkeys / (double)n_qs * (double)p.Hkv * (double)p.D * 2.0 *
+                             (p.dtype == 0 ? 4.0 : 2.0);
+    const double g = (double)p.k1_group_mb * 1048576.0 / fmax(seq_bytes, 1.0);
+    qb_group = g >= (double)n_qs ? (int)n_qs : max(1, (int)g);
+  }
 
   // SM partition for concurrent K1 / K2: P minimising max(prefill time on P SMs, decode
   // time on the other SMs, capped by HBM), from per-SM rates of the two kernels.
@@ -187,6 +209,8 @@ __global__ void __launch_bounds__(kMaxThreads) k5_metadata(Params p) {
     p.hdr[kHdrDecodeCounter] = 0;
     p.hdr[kHdrHintViolation] = n_viol ? 1 : 0;
     p.hdr[kHdrDecodeClaimed] = 0;
+    p.hdr[kHdrQbUniform] = qb_uniform;
+    p.hdr[kHdrQbGroup] = qb_group;
     p.hdr[kHdrPrefillCtas] = P;
   }
 }

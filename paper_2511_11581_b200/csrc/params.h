@@ -19,6 +19,8 @@ enum HdrWord {
   kHdrHintViolation = 8, // K5: 1 if some q_b exceeds the max_query_len hint (the plan may miss it)
   kHdrDecodeClaimed = 9, // 1 once the decode kernel's item queue is empty (two-stream partition: K1
                          // CTAs that find their SM only after that may work on prefill items)
+  kHdrQbUniform = 10,    // > 0: every Q-block sequence has this many Q blocks (K1 claims rank by rank)
+  kHdrQbGroup = 11,      // with kHdrQbUniform: sequences per rank-by-rank claim group
   kHdrWords = 64
 };
 
@@ -53,6 +55,7 @@ struct Params {
   int32_t partition;
   int32_t prefill_ctas_fixed;  // > 0: use this P instead of the model (sweeps)
   float k1_tile_us;            // K1 cost per (128-key tile x 256-row Q block) on one SM
+  int32_t k1_group_mb;         // K1 claim order: K/V megabytes per rank-by-rank sequence group
   float k2_sm_gbs;             // K2 K/V streaming rate of one SM (2 CTAs), GB/s
   float hbm_gbs;               // K2 ceiling: HBM read bandwidth, GB/s
   // strides (elements)

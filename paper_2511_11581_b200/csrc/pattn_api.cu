@@ -596,13 +596,17 @@ pattn_status_t run(const pattn_problem_t* p, const void* q, const void* k_cache,
     }
   }
 
+  // K1 claim order for batches of equal Q-block counts: rank by rank within groups of sequences
+  // holding this much K/V (c3p 8 x 8 MB: 286 -> 262 us serial; unbounded on c5's 32 x 8 MB lost
+  // L2 reuse, 2541 -> 2840 us)
+  k.k1_group_mb = env_int("PATTN_K1_GROUP_MB", 32);
   const bool two = !metadata_only && (s2 != s1) && pl.use_k2 && (pl.use_k1 || pl.use_k4);
   if (two && pl.use_k1) {
     // K1 and K2 run concurrently on disjoint SMs; K5 sizes the split from the batch with a
     // per-SM cost model of the two kernels (measured on B200)
     k.partition = 1;
     k.prefill_ctas_fixed = env_int("PATTN_PREFILL_SMS", 0);
-    k.k1_tile_us = env_float("PATTN_K1_TILE_US", 2.8f);
+    k.k1_tile_us = env_float("PATTN_K1_TILE_US", 2.2f);
     // per-SM decode rate of the partition model: the tree (if measured with this decode kernel) /
     // env value, else the measured default of the decode kernel in use (K2W: 100, K2: 61 GB/s/SM;
     // K2W swept 80 / 90 / 100 on configs 3 and 5: 362.5 / 359.5 / 358.1 us and 2653 / 2635 / 2643 us)

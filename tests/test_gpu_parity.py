@@ -821,3 +821,25 @@ def test_k2w_matrix(case):
                 row = torch.from_numpy(row).to(torch.bfloat16)
                 for h in range(g * G, (g + 1) * G):
                     assert torch.equal(out[s, h], row), (case, b, g, h, t)
+
+
+@pytest.mark.parametrize("G,D", [(4, 128), (8, 128), (4, 64)])
+def test_prefill_claim_groups(G, D, monkeypatch):
+    """Batches whose prefills all have the same number of Q blocks: K1 claims rank by rank within
+    groups of sequences (K5: kHdrQbUniform / kHdrQbGroup).  Every group size -- one sequence, a
+    short last group, all sequences -- must cover every item: oracle parity, and bitwise equal
+    outputs across group sizes (the order moves items between CTAs, not their arithmetic)."""
+    seqs = ((1000, 300), (7, 1), (0, 300), (2500, 300), (3000, 1), (333, 300), (64, 300))
+    w = Workload("claim_groups", seqs, 8 * G, 8, D, 16, "bf16")
+    batch = generate(w, seed=71 + G + D, dist="peaked", poison=True)
+    db = DeviceBatch(batch)
+    outs = []
+    for mb in ("1", "11", "16", "100000"):  # ~5 MB of K/V per sequence: groups of 1, 2, 3, 5
+        monkeypatch.setenv("PATTN_K1_GROUP_MB", mb)
+        outs.append(db.run().clone())
+        if mb == "11":
+            assert_close(out_f64(outs[-1]), O.batch_attention(batch), batch.dtype, f"claim groups G={G} D={D}")
+    s2 = torch.cuda.Stream()
+    outs.append(db.run(stream2=s2).clone())  # two-stream partition, group of 5 (env 100000)
+    for o in outs[1:]:
+        assert torch.equal(outs[0], o)
