@@ -46,6 +46,30 @@ __device__ void block_sum_u64(unsigned long long (&v)[N], unsigned long long (*s
   __syncthreads();
 }
 
+// K1 (Q block, 128-key tile) pairs of one Q-block sequence (the partition model's prefill work):
+// sum over its Q blocks t0 = 0, bq, 2 bq, ... < qb of ceil((ctx + min(t0 + bq, qb)) / 128).
+// K5 is one latency-bound warp chain per 32 sequences, so for BLOCK_Q a power of two <= 128 the
+// sum runs over one period P = 128 / bq of the ceilings (term k + P = term k + 1) instead of
+// every Q block; other BLOCK_Q walk the Q blocks.
+__device__ __forceinline__ unsigned long long qblock_tiles(int ctx, int qb, int bq, int nqb) {
+  unsigned long long s = (unsigned long long)((ctx + qb + 127) >> 7);  // the last (maybe short) Q block
+  const int nf = nqb - 1;                                                // full ones end at ctx + k bq
+  if (nf <= 0) return s;
+  if (bq <= 128 && (bq & (bq - 1)) == 0) {
+    const int lp = 7 - (31 - __clz(bq)), P = 1 << lp, m = nf >> lp, rem = nf - (m << lp);
+    unsigned long long sp = 0, sr = 0;
+    for (int r = 1; r <= P; ++r) {
+      const unsigned long long f = (unsigned long long)((ctx + r * bq + 127) >> 7);
+      sp += f;
+      sr += r <= rem ? f : 0ull;
+    }
+    const unsigned long long mm = (unsigned long long)m;
+    return s + mm * sp + (unsigned long long)P * (mm * (mm - 1) / 2) + sr + (unsigned long long)rem * mm;
+  }
+  for (int k = 1; k <= nf; ++k) s += (unsigned long long)((ctx + k * bq + 127) >> 7);
+  return s;
+}
+
 // Block-wide exclusive scan of two ints per thread at once (x: Q blocks, y: decode
 // segments); returns the exclusive prefixes and writes the block totals.
 __device__ int2 block_exclusive_scan2(int2 v, int2* s_warp, int2* total) {
@@ -92,7 +116,7 @@ __global__ void __launch_bounds__(kMaxThreads) k5_metadata(Params p) {
 
   // pass 1: decode count and total decode KV blocks (+ the partition cost model's inputs:
   // K1 (Q block, 128-key tile) pairs and decode keys)
-  int q0 = 0, L0 = 0;  // this thread's sequence when one_pass
+  int q0 = 0, L0 = 0, nqb0 = 0;  // this thread's sequence when one_pass (q_b, L_b, Q blocks)
   unsigned long long my_blocks = 0, my_tiles = 0, my_keys = 0, my_dec = 0, my_viol = 0;
   // Q-block sequences: count, sum of their Q blocks, of squares, of their keys
   unsigned long long my_qs = 0, my_nqb = 0, my_nqb2 = 0, my_qkeys = 0;
@@ -107,16 +131,13 @@ __global__ void __launch_bounds__(kMaxThreads) k5_metadata(Params p) {
       my_blocks += (unsigned long long)((L + p.bs - 1) / p.bs);
       my_keys += (unsigned long long)L;
     } else if (qb > 0) {
-      const unsigned long long nqb = (unsigned long long)((qb + p.block_q - 1) / p.block_q);
+      nqb0 = (qb + p.block_q - 1) / p.block_q;
+      const unsigned long long nqb = (unsigned long long)nqb0;
       my_qs += 1;
       my_nqb += nqb;
       my_nqb2 += nqb * nqb;
       my_qkeys += (unsigned long long)L;
-      if (p.partition) {
-        const int ctx = L - qb;
-        for (int t0 = 0; t0 < qb; t0 += p.block_q)
-          my_tiles += (unsigned long long)((ctx + min(t0 + p.block_q, qb) + 127) / 128);
-      }
+      if (p.partition) my_tiles += qblock_tiles(L - qb, qb, p.block_q, nqb0);
     }
   }
   unsigned long long sums[9] = {my_dec, my_viol, my_blocks, my_tiles, my_keys, my_qs, my_nqb, my_nqb2, my_qkeys};
@@ -128,13 +149,13 @@ __global__ void __launch_bounds__(kMaxThreads) k5_metadata(Params p) {
   // block of each before any (r+1)-th last): longest first within the group.  Groups hold as
   // many sequences as fit k1_group_mb of K/V (L2 reuse: all Q blocks of a sequence read its K/V).
   const unsigned long long n_qs = sums[5], s_nqb = sums[6], s_nqb2 = sums[7], s_qkeys = sums[8];
-  const int qb_uniform = (n_qs > 0 && s_nqb2 * n_qs == s_nqb * s_nqb) ? (int)(s_nqb / n_qs) : 0;
+  // (32-bit and float arithmetic: the counts fit, and the group size is a heuristic)
+  const int qb_uniform = (n_qs > 0 && s_nqb2 * n_qs == s_nqb * s_nqb) ? (int)((unsigned)s_nqb / (unsigned)n_qs) : 0;
   int qb_group = 1;
   if (qb_uniform > 0) {
-    const double seq_bytes = (double)s_qkeys / (double)n_qs * (double)p.Hkv * (double)p.D * 2.0 *
-                             (p.dtype == 0 ? 4.0 : 2.0);
-    const double g = (double)p.k1_group_mb * 1048576.0 / fmax(seq_bytes, 1.0);
-    qb_group = g >= (double)n_qs ? (int)n_qs : max(1, (int)g);
+    const float seq_bytes = (float)s_qkeys * (float)(p.Hkv * p.D * 2 * (p.dtype == 0 ? 4 : 2));  // x n_qs
+    const float g = __fdividef((float)p.k1_group_mb * 1048576.f * (float)n_qs, fmaxf(seq_bytes, 1.f));
+    qb_group = g >= (float)n_qs ? (int)n_qs : max(1, (int)g);
   }
 
   // SM partition for concurrent K1 / K2: P minimising max(prefill time on P SMs, decode
@@ -185,7 +206,7 @@ __global__ void __launch_bounds__(kMaxThreads) k5_metadata(Params p) {
         const long long nblk = (L + p.bs - 1) / p.bs;
         cnt.y = (int)((nblk + C - 1) / C);
       } else if (qb > 0) {
-        cnt.x = (qb + p.block_q - 1) / p.block_q;
+        cnt.x = one_pass ? nqb0 : (qb + p.block_q - 1) / p.block_q;
       }
     }
     int2 tot;
