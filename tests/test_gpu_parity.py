@@ -843,3 +843,38 @@ def test_prefill_claim_groups(G, D, monkeypatch):
     outs.append(db.run(stream2=s2).clone())  # two-stream partition, group of 5 (env 100000)
     for o in outs[1:]:
         assert torch.equal(outs[0], o)
+
+
+@pytest.mark.parametrize("hq", [32, 64, 48])  # G = 4, 8, 6: BLOCK_Q 64 and 32 (closed form), 42 (walk)
+def test_partition_model_tile_count(hq, monkeypatch):
+    """K5's SM split from its cost model (k5_metadata.cu): the K1 work term counts (Q block,
+    128-key tile) pairs with a closed form over one period of the ceilings when BLOCK_Q is a
+    power of two.  Recomputed here by walking every Q block (float32 like the kernel; +-1 SM for
+    FMA contraction), on ragged contexts and Q lengths that are not multiples of BLOCK_Q."""
+    from paper_2511_11581_b200 import pattn
+
+    monkeypatch.setenv("PATTN_K1_TILE_US", "2.2")
+    monkeypatch.setenv("PATTN_K2W_SM_GBS", "10")  # low decode rate, no HBM cap: the split lands mid-range,
+    monkeypatch.setenv("PATTN_HBM_GBS", "100000")  # where it moves ~S/4 SMs per unit of relative K1 work
+    S = torch.cuda.get_device_properties(0).multi_processor_count
+    rng = np.random.default_rng(hq)
+    for rep in range(4):
+        pre = [(int(rng.integers(0, 3000)), int(rng.integers(2, 1500))) for _ in range(int(rng.integers(2, 7)))]
+        dec = [(int(rng.integers(1000, 6000)), 1) for _ in range(int(rng.integers(8, 30)))]
+        w = Workload(f"pm{hq}_{rep}", tuple(pre + dec), hq, 8, 128, 16, "bf16")
+        db = DeviceBatch(generate(w, seed=rep, poison=False))
+        ws = torch.zeros(1 << 24, dtype=torch.uint8, device="cuda")
+        db.run(stream2=torch.cuda.Stream(), workspace=ws)
+        bq = int(ws[12:16].view(torch.int32).item())
+        tiles = sum(-(-(c + min(t0 + bq, q)) // 128) for c, q in pre for t0 in range(0, q, bq))
+        keys = sum(c + 1 for c, _ in dec)
+        f = np.float32
+        tp = f(tiles) * f(8) * f(2.2) * f(1e-6)
+        b = f(10) * f(1e9)
+        nbytes = f(keys) * f(8) * f(128) * f(4)
+        cstar = f(S) * tp * b / (tp * b + nbytes)
+        chbm = f(S) - f(100000) / f(10)
+        want = max(1, min(int(max(cstar, chbm) + f(0.5)), S - 1))
+        got = pattn.workspace_prefill_sms(ws)
+        assert abs(got - want) <= 1, (hq, rep, bq, tiles, got, want)
+        assert S // 8 < want < S - S // 8, (hq, rep, want)  # mid-range: sensitive to the tile count
